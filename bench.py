@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark of the DDP Reducer gradient-sync hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload resnet50|bert_large] [--dtype fp32|bf16] [--cap-mib 25]
+
+Metric (BASELINE.json): "exposed grad-sync ms/iter and bucket allreduce bus
+GB/s at 1/2/4/8 B200".  One step = one pass of the whole hot path (§8(a)
+rows a1-a7) over one batch of synthetic gradients already resident in HBM:
+all gradients of the workload become ready in reverse registration order (one
+batched ddp_grads_ready call: the hooks of a backward whose compute takes no
+time), buckets are launched in order (pack x 1/W -> allreduce -> unpack), and
+ddp_finalize_backward closes the pass.  With no backward compute to hide
+behind, the whole sync is exposed: `value` = device ms per step (CUDA events
+on the producer stream, max over ranks), lower is better.  `busbw` reports the
+bucket allreduce bus bandwidth of a 25 MiB bucket (N > 1).  L2 (126 MB) is
+flushed between timed steps by a 256 MiB memset outside the per-step events.
+
+For N > 1 launch with torchrun (one process per GPU); rank 0 prints ONE JSON
+line.  `--impl reference` times the oracle (oracle/, numpy on host cores) on
+a bounded sample of the same workload (the reference arm of this tier).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "exposed grad-sync ms/iter and bucket allreduce bus GB/s at 1/2/4/8 B200"
+MIB = 1 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="resnet50", choices=["resnet50", "bert_large"])
+    ap.add_argument("--dtype", default="fp32", choices=["fp32", "bf16"])
+    ap.add_argument("--cap-mib", type=float, default=25)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--algo", type=int, default=0, help="force DDP_OPT_ALGO (0 auto)")
+    ap.add_argument("--comm-ctas", type=int, default=0)
+    ap.add_argument("--oneshot-max", type=int, default=-1)
+    ap.add_argument("--twoshot-max", type=int, default=-1)
+    return ap.parse_args()
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def workload_name(a):
+    return f"{a.workload}_grads_{a.dtype}_cap{a.cap_mib:g}MiB"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6541.5), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self.t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        import statistics
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------------
+def run_reference(a):
+    """Reference arm: the oracle as it stands, on host cores, rank 0 only."""
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return
+    from oracle.cpu_baseline import time_sync
+    from synth.gen import gen_grads
+    from synth.shapes import numels
+    ns = numels(a.workload)
+    W = max(1, world)
+    r = time_sync(ns, a.dtype, int(a.cap_mib * MIB), W, seed=15704, gen_grads=gen_grads,
+                  max_iters=a.warmup + a.steps, budget_s=120.0)
+    ms = r["sec_per_iter"] * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms/iter", "n_gpus": W,
+        "steps": r["iters"], "warmup": 0, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if a.dtype == "fp32" else "bf16", "data": "synthetic",
+        "config": {"workload": workload_name(a), "params": r["params"], "world_simulated": W},
+        "cpu_baseline": {"value": ms, "unit": "ms/iter", "cores": r["cores"], "kind": "oracle",
+                         "sample": f"{r['iters']} full iterations of oracle.average.simulate_ddp_sync "
+                                   f"(pack x1/W, rank-order fp32 allreduce, unpack) over {W} in-memory replicas"},
+        "e2e": {"value": ms, "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------------
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = env_rank()
+    if world != a.gpus:
+        raise SystemExit(f"--gpus {a.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+
+    from paper_2006_15704_b200 import _lib as L
+    from paper_2006_15704_b200.ddp import GradReducer
+    from synth import device as sdev
+    from synth.shapes import numels
+
+    ns = numels(a.workload)
+    esize = 4 if a.dtype == "fp32" else 2
+    tdt = torch.float32 if a.dtype == "fp32" else torch.bfloat16
+    cap = int(a.cap_mib * MIB)
+    opts = {}
+    if a.algo:
+        opts[L.OPT_ALGO] = a.algo
+    if a.comm_ctas:
+        opts[L.OPT_COMM_CTAS] = a.comm_ctas
+    if a.oneshot_max >= 0:
+        opts[L.OPT_P2P_ONESHOT_MAX] = a.oneshot_max
+    if a.twoshot_max >= 0:
+        opts[L.OPT_P2P_TWOSHOT_MAX] = a.twoshot_max
+    red = GradReducer(ns, a.dtype, cap, options=opts)
+
+    # gradients: views into one flat buffer (256-B aligned params), synthetic, rank-specific
+    offs, pos = [], 0
+    for n in ns:
+        offs.append(pos)
+        pos += (n * esize + 255) // 256 * 256 // esize
+    flat = torch.empty(pos, dtype=tdt, device=dev)
+    grads = [flat[o:o + n] for o, n in zip(offs, ns)]
+    sdev.fill_all(grads, 15704, rank, 0, "normal", a.dtype)
+    order = list(range(len(ns) - 1, -1, -1))
+    batch = L.ReadyBatch(order, [grads[p].data_ptr() for p in order])
+    flush = torch.empty(256 * MIB, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        red.grads_ready(batch, stream)
+        red.finalize(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+
+    def timed(fn, k, pre=None):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        for i in range(k):
+            flush.zero_()
+            if pre:
+                pre()
+            evs[i][0].record(stream)
+            fn()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        return [s.elapsed_time(e) for s, e in evs]
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- main timed region -------------------------------------------------------
+    for _ in range(a.warmup):
+        step()
+    barrier()
+    with ClockSampler(local) as clk:
+        barrier()
+        times = timed(step, a.steps)
+        barrier()
+    ms = max_over_ranks(sum(times) / len(times))
+
+    # ---- per-kernel device time (profile events on the comm stream) -----------------
+    L.ddp_set_option(red.ctx, L.OPT_PROFILE, 1)
+    red.profile_read()
+    kprof_steps = min(10, a.steps)
+    timed(step, kprof_steps)
+    prof = red.profile_read()
+    L.ddp_set_option(red.ctx, L.OPT_PROFILE, 0)
+    algos = red.bucket_algos()
+    bnumel = red.bucket_numels()
+    S_tot = sum(bnumel) * esize
+    launches_per_step = sum(1 if x != "nccl" else 2 for x in algos)
+
+    # dominant kernel roofline
+    peak_hbm, peak_src = measured_peaks()
+    kinds = {k: v for k, v in prof.items() if v[1] > 0}
+    dom = max(kinds, key=lambda k: kinds[k][0]) if kinds else None
+    roof = None
+    if dom is not None:
+        tot_ms, cnt = kinds[dom]
+        avg_ms = tot_ms / cnt
+        n_p2p = sum(1 for x in algos if x != "nccl")
+        if dom == "p2p_fused" and world == 1:
+            # W=1 fused one-shot: pack (2S) + unpack (2S) of every P2P bucket
+            byts = 4 * sum(n * esize for n, x in zip(bnumel, algos) if x != "nccl") / max(1, n_p2p)
+            roof = {"bound": "hbm", "achieved": byts / (avg_ms * 1e-3) / 1e9, "peak": peak_hbm, "unit": "GB/s"}
+        elif dom in ("pack", "unpack"):
+            byts = 2 * sum(n * esize for n, x in zip(bnumel, algos) if x == "nccl") / max(1, len(algos) - n_p2p)
+            roof = {"bound": "hbm", "achieved": byts / (avg_ms * 1e-3) / 1e9, "peak": peak_hbm, "unit": "GB/s"}
+        else:
+            # NVLink bound: 2(W-1)/W * S bytes per direction per GPU (ring / two-shot)
+            sel = [n * esize for n, x in zip(bnumel, algos) if (x == "nccl") == (dom == "nccl_allreduce")]
+            byts = 2 * (world - 1) / world * sum(sel) / max(1, len(sel))
+            roof = {"bound": "nvlink", "achieved": byts / (avg_ms * 1e-3) / 1e9, "peak": 770.0, "unit": "GB/s"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = None
+        roof["kernel"] = dom
+        roof["peak_source"] = peak_src if roof["bound"] == "hbm" else "B200_PROFILING.md peer copy 770 GB/s/dir"
+        roof["avg_launch_ms"] = avg_ms
+
+    # ---- bucket allreduce bus bandwidth on a 25 MiB bucket (N > 1) ------------------
+    busbw = None
+    if world > 1:
+        n25 = 25 * MIB // esize
+        red25 = GradReducer([n25], a.dtype, 25 * MIB, options=opts)
+        g25 = torch.empty(n25, dtype=tdt, device=dev)
+        sdev.fill(g25, 15704, rank, 0, 0, "normal", a.dtype)
+        L.ddp_set_option(red25.ctx, L.OPT_PROFILE, 1)
+
+        def s25():
+            red25.grad_ready(0, g25, stream)
+            red25.finalize(stream)
+        for _ in range(5):
+            s25()
+        red25.profile_read()
+        barrier()
+        timed(s25, 20)
+        p25 = red25.profile_read()
+        t = sum(v[0] for v in p25.values()) / 20   # whole sync of the bucket (pack+AR+unpack or fused)
+        t = max_over_ranks(t)
+        busbw = {"value": 25 * MIB / (t * 1e-3) * 2 * (world - 1) / world / 1e9, "unit": "GB/s",
+                 "bucket_mib": 25, "algo": red25.bucket_algos()[0], "ms": t,
+                 "includes": "pack x1/W + allreduce + unpack"}
+        red25.close()
+
+    # ---- e2e through the public API with host buffers --------------------------------
+    e2e = None
+    if not a.no_e2e:
+        host = torch.empty(flat.numel(), dtype=tdt, pin_memory=True)
+        host.copy_(flat)
+        out = torch.empty_like(host, pin_memory=True)
+
+        def e2e_step():
+            flat.copy_(host, non_blocking=True)
+            step()
+            out.copy_(flat, non_blocking=True)
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        et = timed(e2e_step, max(3, min(a.steps, 20)))
+        e2e = {"value": max_over_ranks(sum(et) / len(et)), "unit": "ms/iter",
+               "h2d_bytes_per_step": flat.numel() * esize, "d2h_bytes_per_step": flat.numel() * esize}
+
+    # ---- host overhead of the per-gradient hook call ----------------------------------
+    t0 = time.perf_counter()
+    for p in order:
+        red.grad_ready(p, grads[p], stream)
+    t1 = time.perf_counter()
+    red.finalize(stream)
+    torch.cuda.synchronize(dev)
+    host_us = (t1 - t0) / len(order) * 1e6
+
+    red.check_errors()
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        from oracle.cpu_baseline import time_sync
+        from synth.gen import gen_grads
+        r = time_sync(ns, a.dtype, cap, 1, seed=15704, gen_grads=gen_grads, max_iters=3, budget_s=30)
+        cpu = {"value": r["sec_per_iter"] * 1e3, "unit": "ms/iter", "cores": r["cores"], "kind": "oracle",
+               "sample": f"{r['iters']} full iterations of oracle simulate_ddp_sync on the same workload (W=1)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": ms, "unit": "ms/iter", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if a.dtype == "fp32" else "bf16",
+            "data": "synthetic (seeded splitmix64 gradients shaped like the workload; no model compute)",
+            "config": {"workload": workload_name(a), "params": sum(ns), "tensors": len(ns),
+                       "buckets": len(bnumel), "bucket_algos": algos, "bucket_cap_mib": a.cap_mib,
+                       "grad_bytes_per_step": S_tot, "l2": "flushed between steps (256 MiB memset outside events)",
+                       "ready_order": "reverse registration, one batched ddp_grads_ready per step",
+                       "parallelism": f"dp{world}"},
+            "busbw": busbw,
+            "roofline": roof,
+            "kernel_ms_per_step": {k: v[0] / kprof_steps for k, v in prof.items() if v[1]},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches_per_step * a.steps,
+            "host_us_per_grad_ready": host_us,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    red.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

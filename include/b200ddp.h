@@ -1,0 +1,177 @@
+/*
+ * b200ddp.h — C ABI of the B200-native DDP Reducer gradient synchronization.
+ *
+ * Implements the hot path of Li et al., "PyTorch Distributed: Experiences on
+ * Accelerating Data Parallel Training" (arXiv 2006.15704), §3.2-§4.2
+ * and Algorithm 1 (L205-L244):
+ *   - bucket assignment in reverse registration order under a byte cap
+ *     (P:L217, L304, L308, L415);
+ *   - one ready signal per gradient (the autograd hook) with a
+ *     pending count per bucket and in-order bucket launch;
+ *   - pack + scale by 1/world into the flat bucket;
+ *   - bucket allreduce on a communication stream overlapping backward
+ *      — NCCL, or a hand-written sm_100a P2P kernel;
+ *   - unpack of the averaged values into the gradients;
+ *   - no_sync accumulation.
+ *
+ * Conventions (all functions):
+ *   - Every call returns a ddp_status_t; no C++ exception crosses the ABI.
+ *     ddp_last_error() returns a thread-local message for the last failure.
+ *   - A context is single-threaded: calls come from the one autograd device
+ *     thread (or a bench loop).
+ *   - "stream" arguments are cudaStream_t values passed as void* (NULL = the
+ *     legacy default stream).  Device pointers are plain CUDA device
+ *     addresses on the bound device.
+ *   - Ownership: param_numel is copied at create.  Gradient buffers passed to
+ *     ddp_grad_ready are BORROWED and must stay valid (and must not be written
+ *     by the caller) until the consumer stream passes the wait enqueued by
+ *     ddp_finalize_backward; they are re-supplied every pass because .grad may
+ *     be reallocated between iterations.  Symmetric storage passed to
+ *     ddp_bind_device is caller-allocated and must outlive the context.  The
+ *     library owns its NCCL communicator, CUDA events and tables.
+ *   - State machine: CREATED -> (bind) -> IDLE <-> IN_PASS.  The first
+ *     ddp_grad_ready of a pass opens it; ddp_finalize_backward closes it.
+ *     A CUDA or NCCL failure, a peer timeout or DDP_ERR_INCOMPLETE poisons
+ *     the context: every later call returns DDP_ERR_POISONED.
+ */
+#ifndef B200DDP_H
+#define B200DDP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ddp_ctx ddp_ctx_t; /* opaque, library-owned */
+
+typedef enum { DDP_FP32 = 0, DDP_BF16 = 1 } ddp_dtype_t;
+
+typedef enum {
+  DDP_OK = 0,
+  DDP_ERR_INVALID_ARG = 1, /* bad argument; context unchanged */
+  DDP_ERR_STATE = 2,       /* call not legal in the current state (e.g. nested no_sync) */
+  DDP_ERR_DUPLICATE = 3,   /* param marked ready twice in one pass */
+  DDP_ERR_INCOMPLETE = 4,  /* finalize with params never ready (P:L199 hang) — poisons */
+  DDP_ERR_CUDA = 5,        /* CUDA runtime error — poisons */
+  DDP_ERR_NCCL = 6,        /* NCCL error — poisons */
+  DDP_ERR_NOMEM = 7,       /* host allocation failed */
+  DDP_ERR_POISONED = 8,    /* context poisoned by an earlier fatal error */
+  DDP_ERR_TIMEOUT = 9,     /* a peer never reached a P2P barrier — poisons */
+  DDP_ERR_UNSUPPORTED = 10 /* feature not available in this build / state */
+} ddp_status_t;
+
+/* Option keys for ddp_set_option / ddp_get_option (legal in CREATED or IDLE;
+ * every rank must use identical values, because the algorithm choice and the
+ * P2P grid shape must agree across ranks). */
+enum {
+  DDP_OPT_OVERLAP = 1,          /* 1 (default): launch buckets from the hooks; 0: launch all at
+                                   finalize — the non-overlapped baseline of P:L164-L175 / L399 */
+  DDP_OPT_P2P_ONESHOT_MAX = 2,  /* buckets <= this many bytes use the one-shot P2P kernel */
+  DDP_OPT_P2P_TWOSHOT_MAX = 3,  /* buckets <= this many bytes use the two-shot P2P kernel; larger
+                                   buckets use NCCL */
+  DDP_OPT_COMM_CTAS = 4,        /* max CTAs of a P2P kernel when world > 1 (1..148) */
+  DDP_OPT_DRY_RUN = 5,          /* 1: protocol only, no device work (host tests; CREATED only) */
+  DDP_OPT_PROFILE = 6,          /* 1: time every device launch with CUDA events */
+  DDP_OPT_ALGO = 7,             /* force the bucket allreduce: 0 auto, 1 NCCL, 2 one-shot, 3 two-shot */
+  DDP_OPT_PACK_CTAS = 8         /* max CTAs of pack/unpack kernels and of P2P kernels at world 1 */
+};
+
+/* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO. */
+enum { DDP_ALGO_AUTO = 0, DDP_ALGO_NCCL = 1, DDP_ALGO_ONESHOT = 2, DDP_ALGO_TWOSHOT = 3 };
+
+/* ---- construction (host only, deterministic, touches no GPU) -------------
+ * Bucket assignment (Alg. 1 "allocate parameters to buckets in the
+ * reverse order of net.parameters()"; P:L308 cap; P:L415 cap 0 = one bucket
+ * per gradient; reading C-1: a bucket is closed before the parameter that
+ * would push it over bucket_cap_bytes, an oversized parameter sits alone;
+ * C-6: tight packing, offset = running element count).
+ *   param_numel[n_params]: element counts in registration order, each >= 1.
+ *   dtype: DDP_FP32 or DDP_BF16 (one dtype per context, C-11).
+ *   bucket_cap_bytes >= 0.  world >= 1 (<= 8), 0 <= rank < world.
+ * Errors: DDP_ERR_INVALID_ARG, DDP_ERR_NOMEM.  *out untouched on error. */
+ddp_status_t ddp_create(const int64_t* param_numel, int32_t n_params, int32_t dtype,
+                        int64_t bucket_cap_bytes, int32_t world, int32_t rank, ddp_ctx_t** out);
+void ddp_destroy(ddp_ctx_t* ctx); /* NULL-safe; aborts the NCCL comm if poisoned */
+
+/* ---- introspection: the bit-exact mapping contract ---------------------- */
+int32_t ddp_num_buckets(const ddp_ctx_t* ctx); /* -1 if ctx is NULL */
+ddp_status_t ddp_bucket_info(const ddp_ctx_t* ctx, int32_t b, int64_t* numel, int32_t* n_slots);
+/* slot s of bucket b, in scan (reverse registration) order */
+ddp_status_t ddp_bucket_slot(const ddp_ctx_t* ctx, int32_t b, int32_t s, int32_t* param, int64_t* offset);
+ddp_status_t ddp_param_location(const ddp_ctx_t* ctx, int32_t p, int32_t* bucket, int64_t* offset);
+/* Bytes of symmetric storage each rank must allocate (peer-mapped) and pass to
+ * ddp_bind_device; depends on options, so query after ddp_set_option. */
+ddp_status_t ddp_storage_bytes(const ddp_ctx_t* ctx, int64_t* bytes);
+/* Allreduce algorithm chosen for bucket b (DDP_ALGO_*), given current options. */
+ddp_status_t ddp_bucket_algo(const ddp_ctx_t* ctx, int32_t b, int32_t* algo);
+
+/* ---- device binding (once; collective across ranks) ---------------------
+ * ddp_get_nccl_id: rank 0 creates the NCCL unique id (128 bytes); the caller
+ * broadcasts it to all ranks (PAPER.md L278 rendezvous).
+ * ddp_bind_device: creates the NCCL communicator (blocking, collective),
+ * zeroes this rank's barrier flags and synchronizes all ranks once.
+ *   device: CUDA ordinal.  comm_stream: caller-owned stream that carries all
+ *   of the library's device work ("dedicated set of CUDA streams").
+ *   peer_storage[world]: device addresses, valid on `device`, of every rank's
+ *   storage (ddp_storage_bytes each, 256-B aligned, peer-mapped, e.g. torch
+ *   symmetric memory); peer_storage[rank] is this rank's own.
+ *   multicast_ptr: reserved (NVLS), may be NULL.
+ * Errors: DDP_ERR_STATE (already bound), DDP_ERR_INVALID_ARG, DDP_ERR_CUDA,
+ * DDP_ERR_NCCL. */
+ddp_status_t ddp_get_nccl_id(uint8_t out[128]);
+ddp_status_t ddp_bind_device(ddp_ctx_t* ctx, int32_t device, const uint8_t nccl_id[128],
+                             void* comm_stream, void* const* peer_storage, void* multicast_ptr);
+
+/* ---- per-iteration hot path -----------------------------------------------
+ * ddp_grad_ready: the autograd hook.  Marks param_idx
+ * ready for this pass; `grad` is its gradient (param_numel elements of the
+ * context dtype, contiguous, any alignment) produced on `producer_stream`.
+ * When the lowest unlaunched bucket(s) become complete, they are launched in
+ * bucket order on the comm stream after an event wait on the producer
+ * stream(s): pack (x 1/world) -> allreduce -> unpack into the gradients.
+ * Inside no_sync (C-9: sampled at pass open) the call only records readiness.
+ * Errors: DDP_ERR_INVALID_ARG (index / NULL grad), DDP_ERR_DUPLICATE,
+ * DDP_ERR_STATE (not bound and not dry-run), DDP_ERR_CUDA / _NCCL. */
+ddp_status_t ddp_grad_ready(ddp_ctx_t* ctx, int32_t param_idx, void* grad, void* producer_stream);
+/* Batched form: equivalent to n successive ddp_grad_ready calls in array order. */
+ddp_status_t ddp_grads_ready(ddp_ctx_t* ctx, int32_t n, const int32_t* param_idx,
+                             void* const* grads, void* producer_stream);
+/* ddp_finalize_backward: closes the pass ("block waiting for all
+ * AllReduce ops", done asynchronously: the consumer stream waits on the comm
+ * stream, no host block).  Launches any deferred buckets (OVERLAP=0) and
+ * replenishes the pending counts.  Returns DDP_ERR_INCOMPLETE (and
+ * poisons) if some parameter was never ready; DDP_ERR_STATE if no pass is
+ * open.  After it returns, gradients read on consumer_stream hold the
+ * averages. */
+ddp_status_t ddp_finalize_backward(ddp_ctx_t* ctx, void* consumer_stream);
+/* no_sync: legal only between passes; nesting / end without
+ * begin -> DDP_ERR_STATE.  Passes opened inside the scope do no device work;
+ * the caller keeps accumulating .grad, and the first pass after
+ * ddp_no_sync_end synchronizes the accumulated gradients. */
+ddp_status_t ddp_no_sync_begin(ddp_ctx_t* ctx);
+ddp_status_t ddp_no_sync_end(ddp_ctx_t* ctx);
+
+/* ---- measurement / test knobs --------------------------------------------- */
+ddp_status_t ddp_set_option(ddp_ctx_t* ctx, int32_t key, int64_t value);
+ddp_status_t ddp_get_option(const ddp_ctx_t* ctx, int32_t key, int64_t* value);
+/* Launch trace of the most recent pass: bucket indices in launch order and,
+ * for each, the 0-based index (within the pass) of the ready signal that
+ * triggered it (= number of ready signals in the pass if launched at
+ * finalize).  *n receives the count; at most `cap` entries are written. */
+ddp_status_t ddp_launch_trace(const ddp_ctx_t* ctx, int32_t* buckets, int32_t* triggers,
+                              int32_t cap, int32_t* n);
+/* With DDP_OPT_PROFILE=1: synchronizes the recorded events and returns the
+ * summed device milliseconds and launch counts since the last read, per kind
+ * [0]=pack [1]=NCCL allreduce [2]=unpack [3]=fused P2P kernel; then clears. */
+ddp_status_t ddp_profile_read(ddp_ctx_t* ctx, double ms[4], int64_t launches[4]);
+/* Checks the device-side error word (P2P barrier timeout). */
+ddp_status_t ddp_check_device_errors(ddp_ctx_t* ctx);
+const char* ddp_last_error(void);
+/* Library version string. */
+const char* ddp_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200DDP_H */

@@ -1,0 +1,687 @@
+// reducer.cpp — host core of the B200-native DDP Reducer (C ABI in
+// include/b200ddp.h).  Plays the role of the paper's reducer.cpp (PAPER.md
+// §4.2): parameter-to-bucket map, per-gradient ready tracking
+// (the autograd-hook entry point), in-order bucket launch on a dedicated
+// communication stream, finalize; plus no_sync (§3.2.4).
+//
+// Device work per launched bucket b, all on the comm stream after an event
+// wait on the producer stream(s) (overlap with backward):
+//   P2P (one-/two-shot):  ONE fused kernel: pack x 1/W -> exchange -> unpack
+//   NCCL:                 pack kernel -> ncclAllReduce(sum) -> unpack kernel
+// The choice is a deterministic function of bucket bytes and options, so it
+// is identical on every rank (same order and content on all ranks).
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../internal.h"
+#include "b200ddp.h"
+#include "b200ddp_emu.h"
+
+using namespace b200ddp;
+
+namespace {
+
+thread_local std::string g_err;
+
+ddp_status_t fail(ddp_status_t st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+constexpr int64_t kMinChunkElems = 4096;   // smallest per-CTA chunk worth a CTA
+constexpr int64_t kBarrierScratch = 32 * 1024;  // scratch int inside the flags region
+
+struct Bucket {
+  int64_t numel = 0;
+  std::vector<int32_t> params;  // slot -> param, scan (reverse registration) order
+  std::vector<int64_t> off;     // slot offsets, n+1 entries
+  std::vector<void*> grads;     // slot -> gradient pointer supplied this pass
+  int64_t byte_off = 0;         // inside the symmetric storage
+  int algo = DDP_ALGO_NCCL;
+  int ctas = 1;
+  int64_t shard = 0, chunk = 0;
+};
+
+enum class State { CREATED, IDLE, IN_PASS };
+
+struct ProfRec {
+  int kind;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct ddp_ctx {
+  // configuration
+  int32_t world = 1, rank = 0, dtype = 0, esize = 4;
+  int64_t cap = 0;
+  std::vector<int64_t> numel;
+  std::vector<Bucket> buckets;
+  std::vector<int32_t> p_bucket, p_slot;
+  std::vector<int64_t> p_off;
+  // options
+  int64_t overlap = 1, oneshot_max = 256 * 1024, twoshot_max = INT64_MAX, comm_ctas = 32,
+          dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 4;
+  // symmetric storage layout (bytes)
+  int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
+          stage1_stride = 0, storage_bytes = 0;
+  // protocol state
+  State state = State::CREATED;
+  bool bound = false, emulated = false, poisoned = false;
+  bool no_sync = false, pass_no_sync = false;
+  std::vector<uint8_t> ready;
+  std::vector<int32_t> pending;
+  int32_t cursor = 0, n_ready = 0;
+  std::vector<std::pair<int32_t, int32_t>> trace, last_trace;
+  // device state
+  int device = -1;
+  cudaStream_t comm = nullptr;
+  ncclComm_t nccl = nullptr;
+  void* storage[kMaxWorld] = {};
+  int64_t grad_rank_stride = 0;
+  std::vector<cudaStream_t> unwaited;  // producer streams since the last event wait
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> stream_events;
+  cudaEvent_t comm_done = nullptr;
+  uint32_t p2p_seq = 1;
+  uint64_t p2p_launches = 0;
+  uint32_t* err_host = nullptr;
+  uint32_t* err_dev = nullptr;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> event_pool;
+};
+
+namespace {
+
+ddp_status_t cuda_fail(ddp_ctx* c, cudaError_t e, const char* what) {
+  if (c) c->poisoned = true;
+  return fail(DDP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+ddp_status_t nccl_fail(ddp_ctx* c, ncclResult_t r, const char* what) {
+  if (c) c->poisoned = true;
+  return fail(DDP_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+#define CUDA_TRY(c, expr)                                   \
+  do {                                                      \
+    cudaError_t _e = (expr);                                \
+    if (_e != cudaSuccess) return cuda_fail((c), _e, #expr); \
+  } while (0)
+#define NCCL_TRY(c, expr)                                   \
+  do {                                                      \
+    ncclResult_t _r = (expr);                               \
+    if (_r != ncclSuccess) return nccl_fail((c), _r, #expr); \
+  } while (0)
+
+// ---- a1: bucket assignment (readings C-1, C-6) ----
+void assign(ddp_ctx* c) {
+  const int n = (int)c->numel.size();
+  c->buckets.clear();
+  Bucket cur;
+  for (int p = n - 1; p >= 0; --p) {
+    if (!cur.params.empty() && (cur.numel + c->numel[p]) * c->esize > c->cap) {
+      c->buckets.push_back(std::move(cur));
+      cur = Bucket();
+    }
+    cur.params.push_back(p);
+    cur.off.push_back(cur.numel);
+    cur.numel += c->numel[p];
+  }
+  c->buckets.push_back(std::move(cur));
+  c->p_bucket.assign(n, -1);
+  c->p_slot.assign(n, -1);
+  c->p_off.assign(n, -1);
+  for (int b = 0; b < (int)c->buckets.size(); ++b) {
+    Bucket& bk = c->buckets[b];
+    bk.off.push_back(bk.numel);
+    bk.grads.assign(bk.params.size(), nullptr);
+    for (int s = 0; s < (int)bk.params.size(); ++s) {
+      c->p_bucket[bk.params[s]] = b;
+      c->p_slot[bk.params[s]] = s;
+      c->p_off[bk.params[s]] = bk.off[s];
+    }
+  }
+}
+
+int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
+  const int64_t bytes = bk.numel * c->esize;
+  int a;
+  if (c->algo != DDP_ALGO_AUTO) a = (int)c->algo;
+  else if (c->world == 1) a = DDP_ALGO_ONESHOT;
+  else if (bytes <= c->oneshot_max) a = DDP_ALGO_ONESHOT;
+  else if (bytes <= c->twoshot_max) a = DDP_ALGO_TWOSHOT;
+  else a = DDP_ALGO_NCCL;
+  if (a != DDP_ALGO_NCCL && (int)bk.params.size() > kMaxSlotsPerLaunch) a = DDP_ALGO_NCCL;
+  return a;
+}
+
+// Grid of a P2P launch: per-CTA chunks of >= kMinChunkElems, 256-element aligned.
+void grid_for(const ddp_ctx* c, Bucket& bk, int max_ctas) {
+  if (bk.algo == DDP_ALGO_NCCL) {
+    bk.ctas = 0;
+    bk.shard = bk.chunk = 0;
+    return;
+  }
+  const int64_t L = bk.algo == DDP_ALGO_TWOSHOT ? align_up(cdiv(bk.numel, c->world), kAlignElems)
+                                                 : align_up(bk.numel, kAlignElems);
+  int64_t C = std::min<int64_t>(max_ctas, std::max<int64_t>(1, cdiv(L, kMinChunkElems)));
+  const int64_t Q = align_up(cdiv(L, C), kAlignElems);
+  C = std::max<int64_t>(1, cdiv(L, Q));
+  bk.shard = L;
+  bk.chunk = Q;
+  bk.ctas = (int)C;
+}
+
+int max_ctas_for(const ddp_ctx* c, const Bucket& bk) {
+  int m = c->world == 1 ? (int)c->pack_ctas : (int)std::min<int64_t>(c->comm_ctas, kMaxCtas);
+  if (c->emulated) {
+    const int e = emulated_max_ctas(bk.algo, c->dtype, (int)bk.params.size(), c->world);
+    m = std::min(m, std::max(1, e));
+  }
+  return std::max(1, m);
+}
+
+void plan(ddp_ctx* c) {
+  int64_t pos = kFlagsBytes;
+  c->flags_off = 0;
+  c->buckets_off = pos;
+  int64_t l2max = 0, n1max = 0;
+  for (Bucket& bk : c->buckets) {
+    bk.algo = resolve_algo(c, bk);
+    bk.byte_off = pos;
+    pos += align_up(bk.numel * c->esize, 256);
+    if (bk.algo == DDP_ALGO_TWOSHOT) l2max = std::max(l2max, align_up(cdiv(bk.numel, c->world), kAlignElems));
+    if (bk.algo == DDP_ALGO_ONESHOT) n1max = std::max(n1max, align_up(bk.numel, kAlignElems));
+  }
+  c->stage2_stride = align_up(l2max * c->esize, 256);
+  c->stage2_off = pos;
+  pos += c->world * c->stage2_stride;
+  c->stage1_stride = align_up(n1max * c->esize, 256);
+  c->stage1_off = pos;
+  pos += 2 * c->world * c->stage1_stride;  // double-buffered by launch parity
+  c->storage_bytes = pos;
+  for (Bucket& bk : c->buckets) grid_for(c, bk, max_ctas_for(c, bk));
+}
+
+void regrid(ddp_ctx* c) {
+  for (Bucket& bk : c->buckets) grid_for(c, bk, max_ctas_for(c, bk));
+}
+
+ddp_status_t check_ctx(const ddp_ctx* c) {
+  if (!c) return fail(DDP_ERR_INVALID_ARG, "null context");
+  if (c->poisoned) return fail(DDP_ERR_POISONED, "context poisoned by an earlier fatal error");
+  return DDP_OK;
+}
+
+// ---- profiling -------------------------------------------------------------
+cudaEvent_t pool_event(ddp_ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+void prof_begin(ddp_ctx* c, int kind) {
+  if (!c->profile) return;
+  ProfRec r{kind, pool_event(c), pool_event(c)};
+  cudaEventRecord(r.a, c->comm);
+  c->prof.push_back(r);
+}
+void prof_end(ddp_ctx* c) {
+  if (!c->profile || c->prof.empty()) return;
+  cudaEventRecord(c->prof.back().b, c->comm);
+}
+
+// ---- a3/a4/a6 device work for one bucket -------------------------------------
+ddp_status_t launch_device(ddp_ctx* c, int b) {
+  Bucket& bk = c->buckets[b];
+  const SlotView sv{bk.off.data(), bk.grads.data(), (int32_t)bk.params.size()};
+  const float scale = 1.0f / (float)c->world;  // fl(1/W), reading C-2
+  char* mine = static_cast<char*>(c->storage[c->rank]);
+  if (bk.algo == DDP_ALGO_NCCL) {
+    void* buf = mine + bk.byte_off;
+    prof_begin(c, 0);
+    CUDA_TRY(c, launch_pack(c->dtype, sv, buf, scale, (int)c->pack_ctas, c->comm));
+    prof_end(c);
+    prof_begin(c, 1);
+    NCCL_TRY(c, ncclAllReduce(buf, buf, (size_t)bk.numel, c->dtype == DDP_FP32 ? ncclFloat32 : ncclBfloat16,
+                              ncclSum, c->nccl, c->comm));
+    prof_end(c);
+    prof_begin(c, 2);
+    CUDA_TRY(c, launch_unpack(c->dtype, sv, buf, (int)c->pack_ctas, c->comm));
+    prof_end(c);
+    return DDP_OK;
+  }
+  P2PLaunch a{};
+  for (int r = 0; r < c->world; ++r) a.storage[r] = c->storage[r];
+  a.flags_byte_off = c->flags_off;
+  a.bucket_byte_off = bk.byte_off;
+  if (bk.algo == DDP_ALGO_TWOSHOT) {
+    a.stage_byte_off = c->stage2_off;
+    a.stage_stride = c->stage2_stride;
+  } else {
+    a.stage_byte_off = c->stage1_off + (int64_t)(c->p2p_launches & 1) * c->world * c->stage1_stride;
+    a.stage_stride = c->stage1_stride;
+  }
+  a.numel = bk.numel;
+  a.shard = bk.shard;
+  a.chunk = bk.chunk;
+  a.world = c->world;
+  a.rank = c->rank;
+  a.ctas = bk.ctas;
+  a.emulated = c->emulated ? 1 : 0;
+  a.seq = c->p2p_seq;
+  a.scale = scale;
+  a.grad_rank_stride = c->grad_rank_stride;
+  a.err = c->err_dev;
+  c->p2p_seq += 2;
+  c->p2p_launches += 1;
+  prof_begin(c, 3);
+  CUDA_TRY(c, launch_p2p(bk.algo, c->dtype, sv, a, c->comm));
+  prof_end(c);
+  return DDP_OK;
+}
+
+// ---- a2/a5: launch bucket b (in order) ---------------------------------------
+ddp_status_t launch_bucket(ddp_ctx* c, int b, int32_t trigger) {
+  c->trace.emplace_back(b, trigger);
+  if (c->dry_run) return DDP_OK;
+  // comm stream waits for everything the producers enqueued so far
+  for (cudaStream_t s : c->unwaited) {
+    cudaEvent_t ev = nullptr;
+    for (auto& se : c->stream_events)
+      if (se.first == s) ev = se.second;
+    if (!ev) {
+      CUDA_TRY(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      c->stream_events.emplace_back(s, ev);
+    }
+    CUDA_TRY(c, cudaEventRecord(ev, s));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->comm, ev, 0));
+  }
+  c->unwaited.clear();
+  return launch_device(c, b);
+}
+
+void open_pass(ddp_ctx* c) {
+  c->state = State::IN_PASS;
+  c->pass_no_sync = c->no_sync;  // reading C-9
+  std::fill(c->ready.begin(), c->ready.end(), 0);
+  for (size_t b = 0; b < c->buckets.size(); ++b) c->pending[b] = (int32_t)c->buckets[b].params.size();
+  c->cursor = 0;
+  c->n_ready = 0;
+  c->trace.clear();
+}
+
+ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s) {
+  if (p < 0 || p >= (int32_t)c->numel.size()) return fail(DDP_ERR_INVALID_ARG, "param index out of range");
+  if (!grad && !c->dry_run) return fail(DDP_ERR_INVALID_ARG, "null gradient pointer");
+  if (c->state != State::IN_PASS) open_pass(c);
+  if (c->ready[p]) return fail(DDP_ERR_DUPLICATE, "param " + std::to_string(p) + " marked ready twice");
+  c->ready[p] = 1;
+  const int32_t t = c->n_ready++;
+  const int32_t b = c->p_bucket[p];
+  c->buckets[b].grads[c->p_slot[p]] = grad;
+  c->pending[b] -= 1;  // P:L306 pending count
+  if (c->pass_no_sync) return DDP_OK;  // hooks disabled
+  if (std::find(c->unwaited.begin(), c->unwaited.end(), s) == c->unwaited.end()) c->unwaited.push_back(s);
+  if (!c->overlap) return DDP_OK;
+  const int32_t nb = (int32_t)c->buckets.size();
+  while (c->cursor < nb && c->pending[c->cursor] == 0) {
+    ddp_status_t st = launch_bucket(c, c->cursor, t);
+    if (st != DDP_OK) return st;
+    c->cursor++;
+  }
+  return DDP_OK;
+}
+
+bool is_layout_key(int32_t k) {
+  return k == DDP_OPT_P2P_ONESHOT_MAX || k == DDP_OPT_P2P_TWOSHOT_MAX || k == DDP_OPT_ALGO;
+}
+
+}  // namespace
+
+// =============================== C ABI ========================================
+extern "C" {
+
+const char* ddp_last_error(void) { return g_err.c_str(); }
+const char* ddp_version(void) { return "b200ddp 0.1 (sm_100a)"; }
+
+ddp_status_t ddp_create(const int64_t* param_numel, int32_t n_params, int32_t dtype,
+                        int64_t bucket_cap_bytes, int32_t world, int32_t rank, ddp_ctx_t** out) {
+  if (!out || !param_numel || n_params < 1) return fail(DDP_ERR_INVALID_ARG, "need >= 1 parameter");
+  if (dtype != DDP_FP32 && dtype != DDP_BF16) return fail(DDP_ERR_INVALID_ARG, "dtype must be FP32 or BF16");
+  if (bucket_cap_bytes < 0) return fail(DDP_ERR_INVALID_ARG, "bucket_cap_bytes < 0");
+  if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
+    return fail(DDP_ERR_INVALID_ARG, "need 1 <= world <= 8 and 0 <= rank < world");
+  for (int32_t i = 0; i < n_params; ++i)
+    if (param_numel[i] < 1) return fail(DDP_ERR_INVALID_ARG, "param numel must be >= 1");
+  ddp_ctx* c = new (std::nothrow) ddp_ctx();
+  if (!c) return fail(DDP_ERR_NOMEM, "out of host memory");
+  try {
+    c->world = world;
+    c->rank = rank;
+    c->dtype = dtype;
+    c->esize = dtype == DDP_FP32 ? 4 : 2;
+    c->cap = bucket_cap_bytes;
+    c->numel.assign(param_numel, param_numel + n_params);
+    assign(c);
+    c->ready.assign(n_params, 0);
+    c->pending.assign(c->buckets.size(), 0);
+    plan(c);
+  } catch (const std::bad_alloc&) {
+    delete c;
+    return fail(DDP_ERR_NOMEM, "out of host memory");
+  }
+  *out = c;
+  return DDP_OK;
+}
+
+void ddp_destroy(ddp_ctx_t* c) {
+  if (!c) return;
+  if (c->bound && !c->emulated) {
+    if (!c->poisoned && c->comm) cudaStreamSynchronize(c->comm);
+    if (c->nccl) {
+      if (c->poisoned) ncclCommAbort(c->nccl);
+      else ncclCommDestroy(c->nccl);
+    }
+  } else if (c->bound && c->comm && !c->poisoned) {
+    cudaStreamSynchronize(c->comm);
+  }
+  for (auto& se : c->stream_events) cudaEventDestroy(se.second);
+  for (auto& r : c->prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+  if (c->comm_done) cudaEventDestroy(c->comm_done);
+  if (c->err_host) cudaFreeHost(c->err_host);
+  delete c;
+}
+
+int32_t ddp_num_buckets(const ddp_ctx_t* c) { return c ? (int32_t)c->buckets.size() : -1; }
+
+ddp_status_t ddp_bucket_info(const ddp_ctx_t* c, int32_t b, int64_t* numel, int32_t* n_slots) {
+  if (!c || b < 0 || b >= (int32_t)c->buckets.size()) return fail(DDP_ERR_INVALID_ARG, "bad bucket");
+  if (numel) *numel = c->buckets[b].numel;
+  if (n_slots) *n_slots = (int32_t)c->buckets[b].params.size();
+  return DDP_OK;
+}
+
+ddp_status_t ddp_bucket_slot(const ddp_ctx_t* c, int32_t b, int32_t s, int32_t* param, int64_t* offset) {
+  if (!c || b < 0 || b >= (int32_t)c->buckets.size()) return fail(DDP_ERR_INVALID_ARG, "bad bucket");
+  const Bucket& bk = c->buckets[b];
+  if (s < 0 || s >= (int32_t)bk.params.size()) return fail(DDP_ERR_INVALID_ARG, "bad slot");
+  if (param) *param = bk.params[s];
+  if (offset) *offset = bk.off[s];
+  return DDP_OK;
+}
+
+ddp_status_t ddp_param_location(const ddp_ctx_t* c, int32_t p, int32_t* bucket, int64_t* offset) {
+  if (!c || p < 0 || p >= (int32_t)c->numel.size()) return fail(DDP_ERR_INVALID_ARG, "bad param");
+  if (bucket) *bucket = c->p_bucket[p];
+  if (offset) *offset = c->p_off[p];
+  return DDP_OK;
+}
+
+ddp_status_t ddp_storage_bytes(const ddp_ctx_t* c, int64_t* bytes) {
+  if (!c || !bytes) return fail(DDP_ERR_INVALID_ARG, "null argument");
+  *bytes = c->storage_bytes;
+  return DDP_OK;
+}
+
+ddp_status_t ddp_bucket_algo(const ddp_ctx_t* c, int32_t b, int32_t* algo) {
+  if (!c || !algo || b < 0 || b >= (int32_t)c->buckets.size()) return fail(DDP_ERR_INVALID_ARG, "bad bucket");
+  *algo = c->buckets[b].algo;
+  return DDP_OK;
+}
+
+ddp_status_t ddp_get_nccl_id(uint8_t out[128]) {
+  if (!out) return fail(DDP_ERR_INVALID_ARG, "null out");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(nullptr, r, "ncclGetUniqueId");
+  std::memcpy(out, &id, 128);
+  return DDP_OK;
+}
+
+static ddp_status_t bind_common(ddp_ctx* c, int32_t device, void* comm_stream) {
+  CUDA_TRY(c, cudaSetDevice(device));
+  c->device = device;
+  c->comm = static_cast<cudaStream_t>(comm_stream);
+  CUDA_TRY(c, cudaHostAlloc(reinterpret_cast<void**>(&c->err_host), sizeof(uint32_t), cudaHostAllocMapped));
+  *c->err_host = 0;
+  CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
+  CUDA_TRY(c, cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming));
+  return DDP_OK;
+}
+
+ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id[128], void* comm_stream,
+                             void* const* peer_storage, void* multicast_ptr) {
+  (void)multicast_ptr;
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (c->bound || c->state != State::CREATED) return fail(DDP_ERR_STATE, "already bound");
+  if (c->dry_run) return fail(DDP_ERR_STATE, "dry-run context cannot be bound");
+  if (!nccl_id || !peer_storage) return fail(DDP_ERR_INVALID_ARG, "null argument");
+  for (int r = 0; r < c->world; ++r) {
+    if (!peer_storage[r] || (reinterpret_cast<uintptr_t>(peer_storage[r]) & 255))
+      return fail(DDP_ERR_INVALID_ARG, "peer storage must be non-null and 256-B aligned");
+    c->storage[r] = peer_storage[r];
+  }
+  if (ddp_status_t st = bind_common(c, device, comm_stream)) return st;
+  ncclUniqueId id;
+  std::memcpy(&id, nccl_id, 128);
+  NCCL_TRY(c, ncclCommInitRank(&c->nccl, c->world, id, c->rank));
+  char* mine = static_cast<char*>(c->storage[c->rank]);
+  CUDA_TRY(c, cudaMemsetAsync(mine + c->flags_off, 0, kFlagsBytes, c->comm));
+  // every rank's flags are zero before anyone's first P2P launch
+  NCCL_TRY(c, ncclAllReduce(mine + kBarrierScratch, mine + kBarrierScratch, 1, ncclInt32, ncclSum, c->nccl, c->comm));
+  CUDA_TRY(c, cudaStreamSynchronize(c->comm));
+  c->bound = true;
+  c->state = State::IDLE;
+  return DDP_OK;
+}
+
+ddp_status_t ddp_bind_emulated(ddp_ctx_t* c, int32_t device, void* comm_stream, void* const* storages,
+                               int64_t grad_rank_stride_bytes) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (c->bound || c->state != State::CREATED) return fail(DDP_ERR_STATE, "already bound");
+  if (c->dry_run) return fail(DDP_ERR_STATE, "dry-run context cannot be bound");
+  if (c->rank != 0) return fail(DDP_ERR_INVALID_ARG, "emulated context must be created with rank 0");
+  if (!storages) return fail(DDP_ERR_INVALID_ARG, "null storages");
+  for (int r = 0; r < c->world; ++r) {
+    if (!storages[r] || (reinterpret_cast<uintptr_t>(storages[r]) & 255))
+      return fail(DDP_ERR_INVALID_ARG, "storages must be non-null and 256-B aligned");
+  }
+  for (const Bucket& bk : c->buckets)
+    if (bk.algo == DDP_ALGO_NCCL) return fail(DDP_ERR_UNSUPPORTED, "emulation runs P2P buckets only (set DDP_OPT_ALGO)");
+  if (ddp_status_t st = bind_common(c, device, comm_stream)) return st;
+  for (int r = 0; r < c->world; ++r) c->storage[r] = storages[r];
+  c->grad_rank_stride = grad_rank_stride_bytes;
+  c->emulated = true;
+  regrid(c);
+  for (int r = 0; r < c->world; ++r)
+    CUDA_TRY(c, cudaMemsetAsync(static_cast<char*>(c->storage[r]) + c->flags_off, 0, kFlagsBytes, c->comm));
+  CUDA_TRY(c, cudaStreamSynchronize(c->comm));
+  c->bound = true;
+  c->state = State::IDLE;
+  return DDP_OK;
+}
+
+ddp_status_t ddp_grad_ready(ddp_ctx_t* c, int32_t p, void* grad, void* producer_stream) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (!c->bound && !c->dry_run) return fail(DDP_ERR_STATE, "context not bound to a device");
+  return grad_ready_one(c, p, grad, static_cast<cudaStream_t>(producer_stream));
+}
+
+ddp_status_t ddp_grads_ready(ddp_ctx_t* c, int32_t n, const int32_t* params, void* const* grads,
+                             void* producer_stream) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (!c->bound && !c->dry_run) return fail(DDP_ERR_STATE, "context not bound to a device");
+  if (n < 0 || (n > 0 && (!params || (!grads && !c->dry_run)))) return fail(DDP_ERR_INVALID_ARG, "bad batch");
+  for (int32_t i = 0; i < n; ++i) {
+    ddp_status_t st = grad_ready_one(c, params[i], grads ? grads[i] : nullptr,
+                                     static_cast<cudaStream_t>(producer_stream));
+    if (st != DDP_OK) return st;
+  }
+  return DDP_OK;
+}
+
+ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (c->state != State::IN_PASS) return fail(DDP_ERR_STATE, "no backward pass is open");
+  if (c->n_ready != (int32_t)c->numel.size()) {
+    c->poisoned = true;  // peers may be blocked in a collective
+    c->last_trace = c->trace;
+    c->state = State::IDLE;
+    return fail(DDP_ERR_INCOMPLETE, std::to_string(c->numel.size() - c->n_ready) +
+                                        " parameter(s) never marked ready in this pass");
+  }
+  if (!c->pass_no_sync) {
+    const int32_t nb = (int32_t)c->buckets.size();
+    while (c->cursor < nb) {  // OVERLAP=0: all launches at finalize, in order
+      ddp_status_t st = launch_bucket(c, c->cursor, c->n_ready);
+      if (st != DDP_OK) return st;
+      c->cursor++;
+    }
+    if (!c->dry_run) {
+      CUDA_TRY(c, cudaEventRecord(c->comm_done, c->comm));
+      CUDA_TRY(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), c->comm_done, 0));
+    }
+  }
+  c->unwaited.clear();
+  for (Bucket& bk : c->buckets) std::fill(bk.grads.begin(), bk.grads.end(), nullptr);
+  c->last_trace = c->trace;
+  c->state = State::IDLE;  // pending counts are replenished at the next pass open
+  return DDP_OK;
+}
+
+ddp_status_t ddp_no_sync_begin(ddp_ctx_t* c) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (c->state == State::IN_PASS) return fail(DDP_ERR_STATE, "no_sync toggled inside a backward pass");
+  if (c->no_sync) return fail(DDP_ERR_STATE, "nested no_sync");
+  c->no_sync = true;
+  return DDP_OK;
+}
+
+ddp_status_t ddp_no_sync_end(ddp_ctx_t* c) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (c->state == State::IN_PASS) return fail(DDP_ERR_STATE, "no_sync toggled inside a backward pass");
+  if (!c->no_sync) return fail(DDP_ERR_STATE, "no_sync_end without no_sync_begin");
+  c->no_sync = false;
+  return DDP_OK;
+}
+
+ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (c->state == State::IN_PASS) return fail(DDP_ERR_STATE, "options cannot change inside a pass");
+  if (is_layout_key(key) && c->bound) return fail(DDP_ERR_STATE, "layout options are fixed once bound");
+  switch (key) {
+    case DDP_OPT_OVERLAP: c->overlap = v ? 1 : 0; return DDP_OK;
+    case DDP_OPT_PROFILE: c->profile = v ? 1 : 0; return DDP_OK;
+    case DDP_OPT_DRY_RUN:
+      if (c->bound) return fail(DDP_ERR_STATE, "dry-run only before binding");
+      c->dry_run = v ? 1 : 0;
+      return DDP_OK;
+    case DDP_OPT_P2P_ONESHOT_MAX:
+      if (v < 0) return fail(DDP_ERR_INVALID_ARG, "negative threshold");
+      c->oneshot_max = v;
+      break;
+    case DDP_OPT_P2P_TWOSHOT_MAX:
+      if (v < 0) return fail(DDP_ERR_INVALID_ARG, "negative threshold");
+      c->twoshot_max = v;
+      break;
+    case DDP_OPT_ALGO:
+      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_TWOSHOT) return fail(DDP_ERR_INVALID_ARG, "bad algo");
+      c->algo = v;
+      break;
+    case DDP_OPT_COMM_CTAS:
+      if (v < 1 || v > 148) return fail(DDP_ERR_INVALID_ARG, "COMM_CTAS must be in [1, 148]");
+      c->comm_ctas = v;
+      regrid(c);
+      return DDP_OK;
+    case DDP_OPT_PACK_CTAS:
+      if (v < 1 || v > 148 * 32) return fail(DDP_ERR_INVALID_ARG, "PACK_CTAS must be in [1, 4736]");
+      c->pack_ctas = v;
+      regrid(c);
+      return DDP_OK;
+    default:
+      return fail(DDP_ERR_INVALID_ARG, "unknown option key");
+  }
+  plan(c);  // layout keys
+  return DDP_OK;
+}
+
+ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
+  if (!c || !v) return fail(DDP_ERR_INVALID_ARG, "null argument");
+  switch (key) {
+    case DDP_OPT_OVERLAP: *v = c->overlap; break;
+    case DDP_OPT_P2P_ONESHOT_MAX: *v = c->oneshot_max; break;
+    case DDP_OPT_P2P_TWOSHOT_MAX: *v = c->twoshot_max; break;
+    case DDP_OPT_COMM_CTAS: *v = c->comm_ctas; break;
+    case DDP_OPT_DRY_RUN: *v = c->dry_run; break;
+    case DDP_OPT_PROFILE: *v = c->profile; break;
+    case DDP_OPT_ALGO: *v = c->algo; break;
+    case DDP_OPT_PACK_CTAS: *v = c->pack_ctas; break;
+    default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
+  }
+  return DDP_OK;
+}
+
+ddp_status_t ddp_launch_trace(const ddp_ctx_t* c, int32_t* buckets, int32_t* triggers, int32_t cap, int32_t* n) {
+  if (!c || !n || cap < 0) return fail(DDP_ERR_INVALID_ARG, "bad argument");
+  const auto& t = c->state == State::IN_PASS ? c->trace : c->last_trace;
+  *n = (int32_t)t.size();
+  for (int32_t i = 0; i < cap && i < (int32_t)t.size(); ++i) {
+    if (buckets) buckets[i] = t[i].first;
+    if (triggers) triggers[i] = t[i].second;
+  }
+  return DDP_OK;
+}
+
+ddp_status_t ddp_profile_read(ddp_ctx_t* c, double ms[4], int64_t launches[4]) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (!ms || !launches) return fail(DDP_ERR_INVALID_ARG, "null argument");
+  for (int k = 0; k < 4; ++k) {
+    ms[k] = 0;
+    launches[k] = 0;
+  }
+  for (auto& r : c->prof) {
+    CUDA_TRY(c, cudaEventSynchronize(r.b));
+    float t = 0;
+    CUDA_TRY(c, cudaEventElapsedTime(&t, r.a, r.b));
+    ms[r.kind] += t;
+    launches[r.kind] += 1;
+    c->event_pool.push_back(r.a);
+    c->event_pool.push_back(r.b);
+  }
+  c->prof.clear();
+  return DDP_OK;
+}
+
+ddp_status_t ddp_check_device_errors(ddp_ctx_t* c) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (c->err_host && *reinterpret_cast<volatile uint32_t*>(c->err_host)) {
+    c->poisoned = true;
+    return fail(DDP_ERR_TIMEOUT, "a peer never reached a P2P barrier (timeout)");
+  }
+  if (c->nccl) {
+    ncclResult_t ar = ncclSuccess;
+    if (ncclCommGetAsyncError(c->nccl, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress)
+      return nccl_fail(c, ar, "NCCL async error");
+  }
+  return DDP_OK;
+}
+
+}  // extern "C"

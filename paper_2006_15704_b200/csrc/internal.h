@@ -1,0 +1,53 @@
+// internal.h — declarations shared by the host core (core/reducer.cpp) and
+// the sm_100a kernels (kernels/*.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace b200ddp {
+
+constexpr int kMaxWorld = 8;
+constexpr int kMaxCtas = 256;                  // rows of the barrier flag table
+constexpr int64_t kFlagsBytes = 64 * 1024;     // >= kMaxCtas * kMaxWorld * 4, 64 KiB aligned
+constexpr int kMaxSlotsPerLaunch = 1024;       // largest by-value slot table
+constexpr int64_t kAlignElems = 256;           // shard / chunk granularity (elements)
+constexpr int kThreads = 512;                  // threads per CTA for every kernel
+
+// Host view of the slots of one bucket (or of a contiguous run of them).
+struct SlotView {
+  const int64_t* off;   // n+1 element offsets inside the bucket; off[n] = end
+  void* const* grad;    // n gradient pointers (rank-0 pointers in emulation)
+  int32_t n;
+};
+
+// Per-launch description of a P2P allreduce (one-shot or two-shot).
+struct P2PLaunch {
+  void* storage[kMaxWorld];   // every rank's symmetric storage base (peer-mapped)
+  int64_t flags_byte_off;     // barrier flags: uint32 [kMaxCtas][kMaxWorld], [cta][src rank]
+  int64_t bucket_byte_off;    // this bucket inside the bucket region
+  int64_t stage_byte_off;     // staging region for this launch (parity applied)
+  int64_t stage_stride;       // bytes between per-source staging slots
+  int64_t numel;              // bucket elements
+  int64_t shard;              // two-shot shard length L (elements); unused by one-shot
+  int64_t chunk;              // per-CTA chunk Q (elements)
+  int32_t world;
+  int32_t rank;               // this rank (ignored when emulated: rank = blockIdx.y)
+  int32_t ctas;               // gridDim.x
+  int32_t emulated;
+  uint32_t seq;               // barrier values seq (first) and seq+1 (second)
+  float scale;                // fl(1/world)
+  int64_t grad_rank_stride;   // emulation: byte distance between ranks' gradients
+  uint32_t* err;              // device-visible error word (mapped pinned host memory)
+};
+
+// dtype: 0 = fp32, 1 = bf16 (ddp_dtype_t).
+cudaError_t launch_pack(int dtype, const SlotView& sv, void* bucket, float scale, int max_ctas,
+                        cudaStream_t s);
+cudaError_t launch_unpack(int dtype, const SlotView& sv, const void* bucket, int max_ctas,
+                          cudaStream_t s);
+cudaError_t launch_p2p(int algo, int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
+// Largest number of CTAs per rank an emulated launch of `world` ranks may use.
+int emulated_max_ctas(int algo, int dtype, int n_slots, int world);
+
+}  // namespace b200ddp

@@ -1,0 +1,224 @@
+// common.cuh — device helpers for the sm_100a DDP kernels: 128-bit vector
+// access, fp32/bf16 lane conversion, and the CTA-cooperative multi-source /
+// multi-destination transfer used by pack, the P2P reduction
+// and unpack.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../internal.h"
+
+namespace b200ddp {
+
+// Slot table passed BY VALUE (__grid_constant__): the gradients of one bucket
+// (or of a run of its slots) and their element offsets inside the bucket.
+template <int MAXS>
+struct SlotArgs {
+  void* grad[MAXS];
+  int64_t off[MAXS + 1];
+  int32_t n;
+};
+
+// ---- 128-bit memory access -------------------------------------------------
+// Gradients are not written by anyone while a kernel reads them: read-only path.
+__device__ __forceinline__ uint4 ld_nc_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+// Staging / bucket data written by peers during the kernel: L2-coherent load.
+__device__ __forceinline__ uint4 ld_cg_v4(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_v4(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w) : "memory");
+}
+
+// ---- element conversions (fp32 accumulate, RNE back; reading C-4) ----------
+template <typename T> struct Elem;
+template <> struct Elem<float> {
+  static constexpr int VE = 4;  // elements per 16 bytes
+  __device__ static __forceinline__ float to_f(float x) { return x; }
+  __device__ static __forceinline__ float from_f(float x) { return x; }
+  __device__ static __forceinline__ void unpack(const uint4& v, float (&f)[8]) {
+    f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
+    f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+  }
+  __device__ static __forceinline__ uint4 pack(const float (&f)[8]) {
+    return make_uint4(__float_as_uint(f[0]), __float_as_uint(f[1]), __float_as_uint(f[2]),
+                      __float_as_uint(f[3]));
+  }
+};
+template <> struct Elem<__nv_bfloat16> {
+  static constexpr int VE = 8;
+  __device__ static __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+  __device__ static __forceinline__ __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
+  __device__ static __forceinline__ void unpack(const uint4& v, float (&f)[8]) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+  }
+  __device__ static __forceinline__ uint4 pack(const float (&f)[8]) {
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t lo = __bfloat16_as_ushort(__float2bfloat16_rn(f[2 * i]));
+      const uint32_t hi = __bfloat16_as_ushort(__float2bfloat16_rn(f[2 * i + 1]));
+      w[i] = lo | (hi << 16);
+    }
+    return make_uint4(w[0], w[1], w[2], w[3]);
+  }
+};
+
+// ---- CTA-cooperative transfer ------------------------------------------------
+// For i in [0, n):  y = sum_{k<ns} src_k[i]  (fp32, in k order; one term when
+// ns == 1), optionally y = fl(y * s), then dst_j[i] = RNE_T(y) for j < nd.
+// Vectorized (16 B) when every pointer has the same address mod 16, with a
+// scalar head/tail; scalar otherwise.  SRC_NC: sources are read-only for the
+// kernel's lifetime (gradients) -> non-coherent path; else L2-coherent loads
+// (data written by peers inside the kernel).  NS_MAX: compile-time bound on
+// ns; single-source transfers keep U = 4 vectors in flight per thread,
+// multi-source ones keep ns.
+template <typename T, int NS_MAX, bool SRC_NC, bool SCALE>
+__device__ __forceinline__ void cta_xfer(T* const (&dst)[kMaxWorld], int nd,
+                                         const T* const (&src)[kMaxWorld], int ns, int64_t n,
+                                         float s) {
+  using E = Elem<T>;
+  constexpr int VE = E::VE;
+  constexpr int U = NS_MAX == 1 ? 4 : 1;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (n <= 0) return;
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(dst[0]) & 15;
+  uintptr_t mis = 0;
+#pragma unroll
+  for (int j = 0; j < kMaxWorld; ++j)
+    if (j < nd) mis |= (reinterpret_cast<uintptr_t>(dst[j]) & 15) ^ a0;
+#pragma unroll
+  for (int k = 0; k < NS_MAX; ++k)
+    if (k < ns) mis |= (reinterpret_cast<uintptr_t>(src[k]) & 15) ^ a0;
+
+  auto ld1 = [&](const T* p) -> float { return E::to_f(SRC_NC ? __ldg(p) : __ldcg(p)); };
+  auto scalar = [&](int64_t i) {
+    float acc = ld1(src[0] + i);
+#pragma unroll
+    for (int k = 1; k < NS_MAX; ++k)
+      if (k < ns) acc = __fadd_rn(acc, ld1(src[k] + i));
+    if (SCALE) acc = __fmul_rn(acc, s);
+    const T y = E::from_f(acc);
+#pragma unroll
+    for (int j = 0; j < kMaxWorld; ++j)
+      if (j < nd) dst[j][i] = y;
+  };
+
+  if (mis != 0) {
+    for (int64_t i = tid; i < n; i += nt) scalar(i);
+    return;
+  }
+  int64_t head = a0 ? (int64_t)((16 - a0) / sizeof(T)) : 0;
+  if (head > n) head = n;
+  for (int64_t i = tid; i < head; i += nt) scalar(i);
+  const int64_t nv = (n - head) / VE;
+  auto vec = [&](int64_t v, const uint4 (&in)[NS_MAX]) {
+    float acc[8], f[8];
+    E::unpack(in[0], acc);
+#pragma unroll
+    for (int k = 1; k < NS_MAX; ++k)
+      if (k < ns) {
+        E::unpack(in[k], f);
+#pragma unroll
+        for (int e = 0; e < VE; ++e) acc[e] = __fadd_rn(acc[e], f[e]);
+      }
+    if (SCALE) {
+#pragma unroll
+      for (int e = 0; e < VE; ++e) acc[e] = __fmul_rn(acc[e], s);
+    }
+    const uint4 y = E::pack(acc);
+#pragma unroll
+    for (int j = 0; j < kMaxWorld; ++j)
+      if (j < nd) st_v4(dst[j] + head + v * VE, y);
+  };
+  auto ldv = [&](const T* p) -> uint4 { return SRC_NC ? ld_nc_v4(p) : ld_cg_v4(p); };
+  int64_t v = tid;
+  for (; v + (int64_t)(U - 1) * nt < nv; v += (int64_t)U * nt) {
+    uint4 in[U][NS_MAX];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int k = 0; k < NS_MAX; ++k)
+        if (k < ns) in[u][k] = ldv(src[k] + head + (v + (int64_t)u * nt) * VE);
+#pragma unroll
+    for (int u = 0; u < U; ++u) vec(v + (int64_t)u * nt, in[u]);
+  }
+  for (; v < nv; v += nt) {
+    uint4 in[NS_MAX];
+#pragma unroll
+    for (int k = 0; k < NS_MAX; ++k)
+      if (k < ns) in[k] = ldv(src[k] + head + v * VE);
+    vec(v, in);
+  }
+  for (int64_t i = head + nv * VE + tid; i < n; i += nt) scalar(i);
+}
+
+// First slot k with off[k] <= x < off[k+1]  (CTA-uniform binary search).
+template <int MAXS>
+__device__ __forceinline__ int find_slot(const SlotArgs<MAXS>& sa, int64_t x) {
+  int a = 0, b = sa.n - 1;
+  while (a < b) {
+    const int m = (a + b + 1) >> 1;
+    if (sa.off[m] <= x) a = m; else b = m - 1;
+  }
+  return a;
+}
+
+// Pack the bucket range [lo, hi) from the gradients into nd buffers:
+// element x goes to dst_j[x - base], scaled by s (Alg. 1, C-2).
+template <typename T, int MAXS>
+__device__ __forceinline__ void walk_pack(const SlotArgs<MAXS>& sa, int64_t lo, int64_t hi,
+                                          T* const (&dstb)[kMaxWorld], int nd, int64_t base,
+                                          float s, int64_t gstride) {
+  if (lo >= hi) return;
+  for (int k = find_slot(sa, lo); k < sa.n && lo < hi; ++k) {
+    const int64_t s0 = sa.off[k], e = min(hi, sa.off[k + 1]);
+    if (e <= lo) continue;
+    const T* g = reinterpret_cast<const T*>(static_cast<const char*>(sa.grad[k]) + gstride) + (lo - s0);
+    T* d[kMaxWorld];
+    const T* sp[kMaxWorld];
+#pragma unroll
+    for (int j = 0; j < kMaxWorld; ++j) { d[j] = dstb[j] + (lo - base); sp[j] = g; }
+    cta_xfer<T, 1, true, true>(d, nd, sp, 1, e - lo, s);
+    lo = e;
+  }
+}
+
+// Unpack / reduce the bucket range [lo, hi) into the gradients:
+// grad(x) = RNE(sum_k src_k[x - base]) (ns == 1: plain copy back, L246).
+template <typename T, int MAXS>
+__device__ __forceinline__ void walk_unpack(const SlotArgs<MAXS>& sa, int64_t lo, int64_t hi,
+                                            const T* const (&srcb)[kMaxWorld], int ns,
+                                            int64_t base, int64_t gstride) {
+  if (lo >= hi) return;
+  for (int k = find_slot(sa, lo); k < sa.n && lo < hi; ++k) {
+    const int64_t s0 = sa.off[k], e = min(hi, sa.off[k + 1]);
+    if (e <= lo) continue;
+    T* g = reinterpret_cast<T*>(static_cast<char*>(sa.grad[k]) + gstride) + (lo - s0);
+    T* d[kMaxWorld];
+    const T* sp[kMaxWorld];
+#pragma unroll
+    for (int j = 0; j < kMaxWorld; ++j) { d[j] = g; sp[j] = srcb[j] + (lo - base); }
+    if (ns == 1) cta_xfer<T, 1, false, false>(d, 1, sp, 1, e - lo, 1.0f);
+    else cta_xfer<T, kMaxWorld, false, false>(d, 1, sp, ns, e - lo, 1.0f);
+    lo = e;
+  }
+}
+
+}  // namespace b200ddp

@@ -1,0 +1,213 @@
+// p2p.cu — hand-written sm_100a bucket allreduce over NVLink 5 / NVSwitch peer
+// memory, fused with pack (x 1/W) and unpack.  One launch per bucket.
+//
+// What it computes ("gradient summation across all processes",
+// L166 average, Alg. 1): for every element x of bucket b,
+//     grad_r(x) <- RNE( sum_{q=0..W-1} RNE(g_q(x) * fl(1/W)) )   on every rank r,
+// accumulated in fp32 in fixed rank order q = 0..W-1 (readings C-2, C-3, C-4),
+// i.e. exactly oracle O-3b, bit-identical on all ranks.
+//
+// Memory (per rank, symmetric storage, see core/reducer.cpp):
+//   flags    uint32 [kMaxCtas][kMaxWorld]   barrier counters, [cta][src rank]
+//   bucket   per-bucket flat buffers         two-shot all-gather target
+//   staging  [W][...] per-source slots        push targets
+//
+// Two-shot (reduce-scatter + all-gather, 2(W-1)/W * S per direction):
+//   A  CTA c of rank r packs chunk c of every shard j and PUSHES it (remote
+//      st.global.v4) into rank j's staging slot r;
+//   B  barrier among CTA c of all ranks;
+//   C  rank r reduces chunk c of its own shard from its W local staging slots
+//      and pushes the result into every rank's bucket;
+//   D  barrier;
+//   E  rank r unpacks chunk c of every shard from its own bucket into .grad.
+// One-shot (small buckets, latency bound): A pushes the whole chunk c to every
+// rank; B barrier; C each rank reduces chunk c from its W local slots straight
+// into .grad (fused unpack).  Staging is double-buffered by launch parity, so
+// no closing barrier is needed (the next launch's barrier orders reuse).
+//
+// Barriers: per CTA index, monotonic uint32 counters written with
+// st.release.sys into the peer's flag table and polled with ld.acquire.sys;
+// all writers fence.acq_rel.sys first.  A bounded spin (30 s of %globaltimer)
+// sets the error word instead of hanging.  All remote traffic is stores.
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace b200ddp {
+
+namespace {
+
+constexpr uint64_t kTimeoutNs = 30ull * 1000 * 1000 * 1000;
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ uint32_t* flag_ptr(void* storage, int64_t flags_off, int cta, int src) {
+  return reinterpret_cast<uint32_t*>(static_cast<char*>(storage) + flags_off) + cta * kMaxWorld + src;
+}
+
+__device__ __forceinline__ void p2p_barrier(const P2PLaunch& a, int r, uint32_t val) {
+  if (a.world == 1) return;
+  __threadfence_system();  // every thread: its remote stores are visible system-wide
+  __syncthreads();
+  const int t = threadIdx.x;
+  const int c = blockIdx.x;
+  if (t < a.world && t != r) {
+    uint32_t* f = flag_ptr(a.storage[t], a.flags_byte_off, c, r);
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(val) : "memory");
+    const uint32_t* mine = flag_ptr(a.storage[r], a.flags_byte_off, c, t);
+    const uint64_t t0 = globaltimer();
+    while (true) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+      if ((int32_t)(v - val) >= 0) break;
+      if (globaltimer() - t0 > kTimeoutNs) {
+        atomicExch(a.err, 1u);
+        break;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ T* at(void* base, int64_t byte_off) {
+  return reinterpret_cast<T*>(static_cast<char*>(base) + byte_off);
+}
+
+template <typename T, int MAXS>
+__global__ void __launch_bounds__(kThreads, 1)
+    twoshot_kernel(const __grid_constant__ SlotArgs<MAXS> sa, const __grid_constant__ P2PLaunch a) {
+  const int W = a.world;
+  const int r = a.emulated ? (int)blockIdx.y : a.rank;
+  const int64_t gstride = a.emulated ? (int64_t)r * a.grad_rank_stride : 0;
+  const int c = blockIdx.x;
+  const int64_t L = a.shard, N = a.numel;
+  auto chunk_lo = [&](int j) { return min(j * L + min((int64_t)c * a.chunk, L), N); };
+  auto chunk_hi = [&](int j) { return min(j * L + min((int64_t)(c + 1) * a.chunk, L), N); };
+
+  // A: pack + scale, push chunk c of shard j into rank j's staging slot r.
+  for (int i = 1; i <= W; ++i) {
+    const int j = (r + i) % W;  // self last; peers in rotated order
+    T* d[kMaxWorld] = {at<T>(a.storage[j], a.stage_byte_off + (int64_t)r * a.stage_stride)};
+    walk_pack<T, MAXS>(sa, chunk_lo(j), chunk_hi(j), d, 1, j * L, a.scale, gstride);
+  }
+  p2p_barrier(a, r, a.seq);
+
+  // C: reduce own shard chunk from the W local slots (rank order), push result
+  // into every rank's bucket (all-gather), starting with the next peer.
+  {
+    const int64_t lo = chunk_lo(r), hi = chunk_hi(r);
+    if (lo < hi) {
+      const T* src[kMaxWorld];
+      T* dst[kMaxWorld];
+#pragma unroll
+      for (int q = 0; q < kMaxWorld; ++q) {
+        src[q] = at<T>(a.storage[r], a.stage_byte_off + (int64_t)q * a.stage_stride) + (lo - r * L);
+        dst[q] = at<T>(a.storage[(r + 1 + q) % W], a.bucket_byte_off) + lo;
+      }
+      cta_xfer<T, kMaxWorld, false, false>(dst, W, src, W, hi - lo, 1.0f);
+    }
+  }
+  p2p_barrier(a, r, a.seq + 1);
+
+  // E: unpack every shard's chunk c from the local bucket into the gradients.
+  const T* b[kMaxWorld] = {at<T>(a.storage[r], a.bucket_byte_off)};
+  for (int j = 0; j < W; ++j) walk_unpack<T, MAXS>(sa, chunk_lo(j), chunk_hi(j), b, 1, 0, gstride);
+}
+
+template <typename T, int MAXS>
+__global__ void __launch_bounds__(kThreads, 1)
+    oneshot_kernel(const __grid_constant__ SlotArgs<MAXS> sa, const __grid_constant__ P2PLaunch a) {
+  const int W = a.world;
+  const int r = a.emulated ? (int)blockIdx.y : a.rank;
+  const int64_t gstride = a.emulated ? (int64_t)r * a.grad_rank_stride : 0;
+  const int64_t lo = min((int64_t)blockIdx.x * a.chunk, a.numel);
+  const int64_t hi = min(lo + a.chunk, a.numel);
+
+  // A: pack + scale once, push to slot r of every rank (self included).
+  {
+    T* d[kMaxWorld];
+#pragma unroll
+    for (int q = 0; q < kMaxWorld; ++q)
+      d[q] = at<T>(a.storage[(r + 1 + q) % W], a.stage_byte_off + (int64_t)r * a.stage_stride);
+    walk_pack<T, MAXS>(sa, lo, hi, d, W, 0, a.scale, gstride);
+  }
+  p2p_barrier(a, r, a.seq);
+
+  // C: reduce the W local slots in rank order straight into the gradients.
+  const T* s[kMaxWorld];
+#pragma unroll
+  for (int q = 0; q < kMaxWorld; ++q)
+    s[q] = at<T>(a.storage[r], a.stage_byte_off + (int64_t)q * a.stage_stride);
+  walk_unpack<T, MAXS>(sa, lo, hi, s, W, 0, gstride);
+}
+
+template <int MAXS>
+SlotArgs<MAXS> make_args(const SlotView& sv) {
+  SlotArgs<MAXS> a;
+  a.n = sv.n;
+  for (int k = 0; k < sv.n; ++k) {
+    a.grad[k] = sv.grad[k];
+    a.off[k] = sv.off[k];
+  }
+  a.off[sv.n] = sv.off[sv.n];
+  return a;
+}
+
+template <typename T, int MAXS>
+void* kernel_ptr(int algo) {
+  return algo == 3 ? reinterpret_cast<void*>(twoshot_kernel<T, MAXS>)
+                   : reinterpret_cast<void*>(oneshot_kernel<T, MAXS>);
+}
+
+template <typename T, int MAXS>
+cudaError_t run(int algo, const SlotView& sv, const P2PLaunch& a, cudaStream_t st) {
+  const SlotArgs<MAXS> sargs = make_args<MAXS>(sv);
+  P2PLaunch pa = a;
+  void* args[] = {const_cast<SlotArgs<MAXS>*>(&sargs), &pa};
+  void* fn = kernel_ptr<T, MAXS>(algo);
+  if (a.emulated) {
+    return cudaLaunchCooperativeKernel(fn, dim3(a.ctas, a.world), dim3(kThreads), args, 0, st);
+  }
+  return cudaLaunchKernel(fn, dim3(a.ctas), dim3(kThreads), args, 0, st);
+}
+
+template <typename T>
+cudaError_t dispatch(int algo, const SlotView& sv, const P2PLaunch& a, cudaStream_t st) {
+  if (sv.n <= 16) return run<T, 16>(algo, sv, a, st);
+  if (sv.n <= 64) return run<T, 64>(algo, sv, a, st);
+  if (sv.n <= 256) return run<T, 256>(algo, sv, a, st);
+  if (sv.n <= kMaxSlotsPerLaunch) return run<T, 1024>(algo, sv, a, st);
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+int occupancy(int algo, int n_slots) {
+  int blocks = 0;
+  void* fn = n_slots <= 16    ? kernel_ptr<T, 16>(algo)
+             : n_slots <= 64  ? kernel_ptr<T, 64>(algo)
+             : n_slots <= 256 ? kernel_ptr<T, 256>(algo)
+                              : kernel_ptr<T, 1024>(algo);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kThreads, 0) != cudaSuccess) return 0;
+  return blocks;
+}
+
+}  // namespace
+
+cudaError_t launch_p2p(int algo, int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s) {
+  return dtype == 0 ? dispatch<float>(algo, sv, a, s) : dispatch<__nv_bfloat16>(algo, sv, a, s);
+}
+
+int emulated_max_ctas(int algo, int dtype, int n_slots, int world) {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+  const int occ = dtype == 0 ? occupancy<float>(algo, n_slots) : occupancy<__nv_bfloat16>(algo, n_slots);
+  return occ * sms / (world > 0 ? world : 1);
+}
+
+}  // namespace b200ddp

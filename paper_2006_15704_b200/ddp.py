@@ -1,0 +1,191 @@
+"""Python front end (glue only) over the native Reducer.
+
+Mirrors the paper's Python layer (§4.1: constructor
+knobs ``process_group`` / ``bucket_cap_mb``, the ``no_sync`` context manager)
+for the gradient path only.  PyTorch is used for device memory (symmetric
+memory for the peer-mapped bucket storage), streams, the process group that
+carries the NCCL unique id, and the autograd hook mechanism
+(``register_post_accumulate_grad_hook``, the AccumulateGrad post-hook of
+P:L186 / L306).  Every step of the synchronization runs in
+``libb200ddp.so``: this module only marshals arguments.
+"""
+
+from __future__ import annotations
+
+import contextlib
+from typing import Dict, Iterable, List, Optional, Sequence
+
+import torch
+import torch.distributed as dist
+
+from . import _lib as L
+
+MIB = 1 << 20
+_DTYPES = {torch.float32: L.FP32, torch.bfloat16: L.BF16, "fp32": L.FP32, "bf16": L.BF16}
+
+
+def _group_info(group) -> tuple:
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def _broadcast_id(nccl_id: Optional[bytes], rank: int, group, device) -> bytes:
+    """Rank 0's NCCL unique id to every rank through the torch process group
+    (PAPER.md L278 rendezvous).  Works with gloo (CPU) and nccl (CUDA)."""
+    backend = dist.get_backend(group)
+    dev = torch.device("cpu") if backend == "gloo" else device
+    t = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        t.copy_(torch.frombuffer(bytearray(nccl_id), dtype=torch.uint8))
+    dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return bytes(t.cpu().tolist())
+
+
+class GradReducer:
+    """One native Reducer context bound to the current CUDA device.
+
+    ``numels``: per-parameter element counts in registration order.
+    ``options``: {key: value} of ``_lib.OPT_*`` applied before binding (must
+    be identical on every rank).
+    """
+
+    def __init__(self, numels: Sequence[int], dtype="fp32", bucket_cap_bytes: int = 25 * MIB,
+                 group=None, device: Optional[torch.device] = None,
+                 options: Optional[Dict[int, int]] = None, comm_stream: Optional[torch.cuda.Stream] = None):
+        self.rank, self.world = _group_info(group)
+        self.group = group
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.numels = [int(n) for n in numels]
+        self.dtype = _DTYPES[dtype]
+        self.ctx = L.ddp_create(self.numels, self.dtype, bucket_cap_bytes, self.world, self.rank)
+        try:
+            for k, v in (options or {}).items():
+                L.ddp_set_option(self.ctx, k, v)
+            self.storage_bytes = L.ddp_storage_bytes(self.ctx)
+            self.comm_stream = comm_stream or torch.cuda.Stream(device=self.device, priority=-1)
+            nccl_id = L.ddp_get_nccl_id() if self.rank == 0 else None
+            if self.world > 1:
+                nccl_id = _broadcast_id(nccl_id, self.rank, group, self.device)
+                self._storage, peers = self._symmetric_storage()
+            else:
+                self._storage = torch.empty(self.storage_bytes, dtype=torch.uint8, device=self.device)
+                peers = [self._storage.data_ptr()]
+            L.ddp_bind_device(self.ctx, self.device.index, nccl_id, self.comm_stream.cuda_stream, peers)
+        except Exception:
+            L.ddp_destroy(self.ctx)
+            self.ctx = None
+            raise
+
+    def _symmetric_storage(self):
+        import torch.distributed._symmetric_memory as symm_mem
+        t = symm_mem.empty(self.storage_bytes, dtype=torch.uint8, device=self.device)
+        h = symm_mem.rendezvous(t, self.group if self.group is not None else dist.group.WORLD)
+        base = h.buffer_ptrs[self.rank]
+        delta = t.data_ptr() - base
+        self._symm_handle = h
+        return t, [int(p) + delta for p in h.buffer_ptrs]
+
+    # ---- introspection -------------------------------------------------------
+    @property
+    def num_buckets(self) -> int:
+        return L.ddp_num_buckets(self.ctx)
+
+    def bucket_algos(self) -> List[str]:
+        return [L.ALGO_NAMES[L.ddp_bucket_algo(self.ctx, b)] for b in range(self.num_buckets)]
+
+    def bucket_numels(self) -> List[int]:
+        return [L.ddp_bucket_info(self.ctx, b)[0] for b in range(self.num_buckets)]
+
+    # ---- hot path --------------------------------------------------------------
+    def grad_ready(self, param_idx: int, grad: torch.Tensor, stream: Optional[torch.cuda.Stream] = None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        L.ddp_grad_ready(self.ctx, param_idx, grad.data_ptr(), s.cuda_stream)
+
+    def grads_ready(self, batch: "L.ReadyBatch", stream: Optional[torch.cuda.Stream] = None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        L.ddp_grads_ready(self.ctx, batch, s.cuda_stream)
+
+    def finalize(self, stream: Optional[torch.cuda.Stream] = None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        L.ddp_finalize_backward(self.ctx, s.cuda_stream)
+
+    @contextlib.contextmanager
+    def no_sync(self):
+        L.ddp_no_sync_begin(self.ctx)
+        try:
+            yield
+        finally:
+            L.ddp_no_sync_end(self.ctx)
+
+    def set_option(self, key: int, value: int):
+        L.ddp_set_option(self.ctx, key, value)
+
+    def profile_read(self):
+        return L.ddp_profile_read(self.ctx)
+
+    def check_errors(self):
+        L.ddp_check_device_errors(self.ctx)
+
+    def close(self):
+        if self.ctx:
+            L.ddp_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DistributedDataParallel(torch.nn.Module):
+    """Wraps a module; gradients of its parameters are bucketed, averaged across
+    the process group and written back into ``.grad`` during backward.
+
+    Constructor: ``process_group``, ``bucket_cap_mb``
+    (default 25, read as MiB, C-5).  ``broadcast_parameters``: rank 0's
+    parameters are copied to every rank at construction (Alg. 1),
+    via torch's broadcast (plumbing, not the hot path).
+    """
+
+    def __init__(self, module: torch.nn.Module, process_group=None, bucket_cap_mb: float = 25,
+                 broadcast_parameters: bool = True, options: Optional[Dict[int, int]] = None):
+        super().__init__()
+        self.module = module
+        self.params = [p for p in module.parameters() if p.requires_grad]
+        dtypes = {p.dtype for p in self.params}
+        if len(dtypes) != 1:
+            raise ValueError("one gradient dtype per reducer (reading C-11)")
+        if broadcast_parameters and dist.is_available() and dist.is_initialized():
+            with torch.no_grad():
+                for p in self.params:
+                    dist.broadcast(p.data, src=0, group=process_group)
+        self.reducer = GradReducer([p.numel() for p in self.params], dtypes.pop(),
+                                   int(bucket_cap_mb * MIB), group=process_group,
+                                   device=self.params[0].device, options=options)
+        self._pass_open = False
+        self._hooks = [p.register_post_accumulate_grad_hook(self._make_hook(i))
+                       for i, p in enumerate(self.params)]
+
+    def _make_hook(self, idx: int):
+        def hook(p: torch.Tensor):
+            if not self._pass_open:
+                self._pass_open = True
+                # finalize when the autograd engine finishes this backward
+                torch.autograd.Variable._execution_engine.queue_callback(self._finalize)
+            g = p.grad
+            if not g.is_contiguous():
+                raise ValueError("gradients must be contiguous")
+            self.reducer.grad_ready(idx, g)
+        return hook
+
+    def _finalize(self):
+        self._pass_open = False
+        self.reducer.finalize()
+
+    def forward(self, *args, **kwargs):
+        return self.module(*args, **kwargs)
+
+    def no_sync(self):
+        return self.reducer.no_sync()

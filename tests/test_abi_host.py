@@ -1,0 +1,240 @@
+"""Host-side tests of the C ABI (no GPU): the library loads, exports every
+symbol the headers declare, and its integer logic (bucket mapping, ready
+tracking, launch order, state machine) equals the oracle bit-for-bit.
+
+Device work is never issued here: protocol tests use DDP_OPT_DRY_RUN, which
+runs the same tracking code and records the launch trace only."""
+
+import itertools
+import os
+import random
+import re
+
+import pytest
+
+from oracle.assignment import MIB, assign_buckets
+from oracle.protocol import replay
+from paper_2006_15704_b200 import _lib as L
+from synth.shapes import numels
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    syms = set()
+    for h in ("b200ddp.h", "b200ddp_emu.h"):
+        txt = open(os.path.join(ROOT, "include", h)).read()
+        txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+        syms |= set(re.findall(r"\b(ddp_[a-z_]+)\s*\(", txt))
+    return syms
+
+
+def test_library_exports_every_declared_symbol():
+    lib = L.lib()
+    syms = _declared_symbols()
+    assert syms == set(L._SIGS)          # the binding covers exactly the declared ABI
+    for s in sorted(syms):
+        assert hasattr(lib, s), s
+    assert L.ddp_version().startswith("b200ddp")
+
+
+def _mapping(ctx):
+    out = []
+    for b in range(L.ddp_num_buckets(ctx)):
+        n, ns = L.ddp_bucket_info(ctx, b)
+        out.append((n, [L.ddp_bucket_slot(ctx, b, s) for s in range(ns)]))
+    return out
+
+
+def _oracle_mapping(a):
+    return [(a.bucket_numel[b], [(p, o) for p, o in a.buckets[b]]) for b in range(a.num_buckets)]
+
+
+CASES = [("toy", 4, 4096)] + [(m, e, c * MIB) for m in ("resnet50", "bert_large") for e in (4, 2)
+                               for c in (0, 1, 5, 25, 200)]
+
+
+@pytest.mark.parametrize("model,esize,cap", CASES)
+def test_mapping_bit_exact_vs_oracle(model, esize, cap):
+    ns = numels(model)
+    ctx = L.ddp_create(ns, L.FP32 if esize == 4 else L.BF16, cap, 1, 0)
+    try:
+        a = assign_buckets(ns, esize, cap)
+        assert L.ddp_num_buckets(ctx) == a.num_buckets
+        assert _mapping(ctx) == _oracle_mapping(a)
+        for p in range(len(ns)):
+            assert L.ddp_param_location(ctx, p) == (a.param_bucket[p], a.param_offset[p])
+    finally:
+        L.ddp_destroy(ctx)
+
+
+def test_mapping_random_small():
+    rng = random.Random(3)
+    for _ in range(300):
+        ns = [rng.randint(1, 40) for _ in range(rng.randint(1, 10))]
+        esize = rng.choice([4, 2])
+        cap = rng.choice([0, rng.randint(1, 200), 1 << 40])
+        ctx = L.ddp_create(ns, L.FP32 if esize == 4 else L.BF16, cap, 1, 0)
+        try:
+            assert _mapping(ctx) == _oracle_mapping(assign_buckets(ns, esize, cap))
+        finally:
+            L.ddp_destroy(ctx)
+
+
+def _dry_ctx(ns, cap, esize=4, world=1, rank=0):
+    ctx = L.ddp_create(ns, L.FP32 if esize == 4 else L.BF16, cap, world, rank)
+    L.ddp_set_option(ctx, L.OPT_DRY_RUN, 1)
+    return ctx
+
+
+def _run_pass(ctx, order, batched=False):
+    if batched:
+        L.ddp_grads_ready(ctx, L.ReadyBatch(order, [0] * len(order)), 0)
+    else:
+        for p in order:
+            L.ddp_grad_ready(ctx, p, 0, 0)
+    L.ddp_finalize_backward(ctx, 0)
+    return L.ddp_launch_trace(ctx)
+
+
+def test_launch_trace_all_toy_permutations():
+    ns = numels("toy")
+    a = assign_buckets(ns, 4, 4096)
+    ctx = _dry_ctx(ns, 4096)
+    try:
+        for order in itertools.permutations(range(6)):   # 720 passes on one context
+            assert _run_pass(ctx, list(order)) == replay(a, order)
+    finally:
+        L.ddp_destroy(ctx)
+
+
+@pytest.mark.parametrize("model,cap", [("resnet50", 25 * MIB), ("resnet50", 1 * MIB), ("bert_large", 25 * MIB)])
+def test_launch_trace_random_orders(model, cap):
+    ns = numels(model)
+    a = assign_buckets(ns, 4, cap)
+    ctx = _dry_ctx(ns, cap)
+    rng = random.Random(11)
+    try:
+        rev = list(range(len(ns) - 1, -1, -1))
+        assert _run_pass(ctx, rev) == replay(a, rev)
+        assert _run_pass(ctx, rev, batched=True) == replay(a, rev)
+        for _ in range(20):
+            order = list(range(len(ns)))
+            rng.shuffle(order)
+            assert _run_pass(ctx, order) == replay(a, order)
+    finally:
+        L.ddp_destroy(ctx)
+
+
+def test_overlap_off_launches_at_finalize():
+    ns = numels("toy")
+    a = assign_buckets(ns, 4, 4096)
+    ctx = _dry_ctx(ns, 4096)
+    L.ddp_set_option(ctx, L.OPT_OVERLAP, 0)
+    try:
+        assert _run_pass(ctx, [5, 4, 3, 2, 1, 0]) == replay(a, [5, 4, 3, 2, 1, 0], overlap=False)
+    finally:
+        L.ddp_destroy(ctx)
+
+
+def test_no_sync_state_machine():
+    ns = numels("toy")
+    ctx = _dry_ctx(ns, 4096)
+    try:
+        L.ddp_no_sync_begin(ctx)
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_no_sync_begin(ctx)                     # nested
+        assert e.value.status == L.ERR_STATE
+        assert _run_pass(ctx, [5, 4, 3, 2, 1, 0]) == []   # no launches
+        L.ddp_grad_ready(ctx, 5, 0, 0)
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_no_sync_end(ctx)                       # toggle mid-pass (C-9)
+        assert e.value.status == L.ERR_STATE
+        for p in [4, 3, 2, 1, 0]:
+            L.ddp_grad_ready(ctx, p, 0, 0)
+        L.ddp_finalize_backward(ctx, 0)
+        L.ddp_no_sync_end(ctx)
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_no_sync_end(ctx)                       # end without begin
+        assert e.value.status == L.ERR_STATE
+        assert [b for b, _ in _run_pass(ctx, [5, 4, 3, 2, 1, 0])] == [0, 1, 2, 3]
+        L.ddp_no_sync_begin(ctx)                         # empty scope
+        L.ddp_no_sync_end(ctx)
+        assert [b for b, _ in _run_pass(ctx, [5, 4, 3, 2, 1, 0])] == [0, 1, 2, 3]
+    finally:
+        L.ddp_destroy(ctx)
+
+
+def test_duplicate_and_incomplete():
+    ns = numels("toy")
+    ctx = _dry_ctx(ns, 4096)
+    try:
+        L.ddp_grad_ready(ctx, 5, 0, 0)
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_grad_ready(ctx, 5, 0, 0)
+        assert e.value.status == L.ERR_DUPLICATE
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_finalize_backward(ctx, 0)
+        assert e.value.status == L.ERR_INCOMPLETE
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_grad_ready(ctx, 4, 0, 0)
+        assert e.value.status == L.ERR_POISONED
+    finally:
+        L.ddp_destroy(ctx)
+
+
+def test_argument_and_state_errors():
+    with pytest.raises(L.DDPError) as e:
+        L.ddp_create([3, 0], L.FP32, 10, 1, 0)
+    assert e.value.status == L.ERR_INVALID_ARG
+    for bad in (dict(world=0, rank=0), dict(world=2, rank=2), dict(world=9, rank=0)):
+        with pytest.raises(L.DDPError):
+            L.ddp_create([3], L.FP32, 10, **bad)
+    with pytest.raises(L.DDPError):
+        L.ddp_create([3], 7, 10, 1, 0)
+    ctx = L.ddp_create([3, 4], L.FP32, 10, 1, 0)
+    try:
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_grad_ready(ctx, 0, 0, 0)               # not bound, not dry-run
+        assert e.value.status == L.ERR_STATE
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_finalize_backward(ctx, 0)
+        assert e.value.status == L.ERR_STATE
+        with pytest.raises(L.DDPError):
+            L.ddp_set_option(ctx, 999, 1)
+        with pytest.raises(L.DDPError):
+            L.ddp_set_option(ctx, L.OPT_COMM_CTAS, 0)
+        L.ddp_set_option(ctx, L.OPT_DRY_RUN, 1)
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_grad_ready(ctx, 2, 0, 0)
+        assert e.value.status == L.ERR_INVALID_ARG
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_bind_device(ctx, 0, b"\0" * 128, 0, [0])
+        assert e.value.status == L.ERR_STATE
+    finally:
+        L.ddp_destroy(ctx)
+    L.ddp_destroy(0)   # NULL-safe
+
+
+def test_algorithm_selection_and_storage_layout():
+    ns = numels("resnet50")
+    ctx = L.ddp_create(ns, L.FP32, 25 * MIB, 4, 1)
+    try:
+        L.ddp_set_option(ctx, L.OPT_P2P_ONESHOT_MAX, 9 * MIB)
+        L.ddp_set_option(ctx, L.OPT_P2P_TWOSHOT_MAX, 20 * MIB)
+        sizes = [L.ddp_bucket_info(ctx, b)[0] * 4 for b in range(L.ddp_num_buckets(ctx))]
+        want = [L.ALGO_ONESHOT if s <= 9 * MIB else L.ALGO_TWOSHOT if s <= 20 * MIB else L.ALGO_NCCL
+                for s in sizes]
+        assert [L.ddp_bucket_algo(ctx, b) for b in range(len(sizes))] == want
+        total = L.ddp_storage_bytes(ctx)
+        assert total >= sum(sizes) + 64 * 1024
+        L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_NCCL)
+        assert {L.ddp_bucket_algo(ctx, b) for b in range(len(sizes))} == {L.ALGO_NCCL}
+        assert L.ddp_get_option(ctx, L.OPT_ALGO) == L.ALGO_NCCL
+    finally:
+        L.ddp_destroy(ctx)
+    one = L.ddp_create(ns, L.FP32, 25 * MIB, 1, 0)   # world 1: everything one-shot
+    try:
+        assert {L.ddp_bucket_algo(one, b) for b in range(L.ddp_num_buckets(one))} == {L.ALGO_ONESHOT}
+    finally:
+        L.ddp_destroy(one)
