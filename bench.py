@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--algo", type=int, default=0, help="force DDP_OPT_ALGO (0 auto)")
     ap.add_argument("--comm-ctas", type=int, default=0)
+    ap.add_argument("--pack-ctas", type=int, default=0)
     ap.add_argument("--oneshot-max", type=int, default=-1)
     ap.add_argument("--twoshot-max", type=int, default=-1)
     return ap.parse_args()
@@ -169,6 +170,8 @@ def run_ours(a):
         opts[L.OPT_ALGO] = a.algo
     if a.comm_ctas:
         opts[L.OPT_COMM_CTAS] = a.comm_ctas
+    if a.pack_ctas:
+        opts[L.OPT_PACK_CTAS] = a.pack_ctas
     if a.oneshot_max >= 0:
         opts[L.OPT_P2P_ONESHOT_MAX] = a.oneshot_max
     if a.twoshot_max >= 0:

@@ -81,43 +81,38 @@ template <> struct Elem<__nv_bfloat16> {
 };
 
 // ---- CTA-cooperative transfer ------------------------------------------------
-// For i in [0, n):  y = sum_{k<ns} src_k[i]  (fp32, in k order; one term when
-// ns == 1), optionally y = fl(y * s), then dst_j[i] = RNE_T(y) for j < nd.
+// For i in [0, n):  y = sum_{k<NS} src_k[i]  (fp32, in k order; a plain load
+// when NS == 1), optionally y = fl(y * s), then dst_j[i] = RNE_T(y), j < ND.
 // Vectorized (16 B) when every pointer has the same address mod 16, with a
 // scalar head/tail; scalar otherwise.  SRC_NC: sources are read-only for the
 // kernel's lifetime (gradients) -> non-coherent path; else L2-coherent loads
-// (data written by peers inside the kernel).  NS_MAX: compile-time bound on
-// ns; single-source transfers keep U = 4 vectors in flight per thread,
-// multi-source ones keep ns.
-template <typename T, int NS_MAX, bool SRC_NC, bool SCALE>
-__device__ __forceinline__ void cta_xfer(T* const (&dst)[kMaxWorld], int nd,
-                                         const T* const (&src)[kMaxWorld], int ns, int64_t n,
+// (data written by peers inside the kernel).  NS / ND are compile-time so the
+// pointer and value arrays live in registers; U vectors per source are kept
+// in flight per thread (U * NS >= 4).
+template <typename T, int NS, int ND, bool SRC_NC, bool SCALE>
+__device__ __forceinline__ void cta_xfer(T* const (&dst)[ND], const T* const (&src)[NS], int64_t n,
                                          float s) {
   using E = Elem<T>;
   constexpr int VE = E::VE;
-  constexpr int U = NS_MAX == 1 ? 4 : 1;
+  constexpr int U = NS >= 4 ? 1 : 4 / NS;
   const int tid = threadIdx.x, nt = blockDim.x;
   if (n <= 0) return;
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(dst[0]) & 15;
   uintptr_t mis = 0;
 #pragma unroll
-  for (int j = 0; j < kMaxWorld; ++j)
-    if (j < nd) mis |= (reinterpret_cast<uintptr_t>(dst[j]) & 15) ^ a0;
+  for (int j = 0; j < ND; ++j) mis |= (reinterpret_cast<uintptr_t>(dst[j]) & 15) ^ a0;
 #pragma unroll
-  for (int k = 0; k < NS_MAX; ++k)
-    if (k < ns) mis |= (reinterpret_cast<uintptr_t>(src[k]) & 15) ^ a0;
+  for (int k = 0; k < NS; ++k) mis |= (reinterpret_cast<uintptr_t>(src[k]) & 15) ^ a0;
 
   auto ld1 = [&](const T* p) -> float { return E::to_f(SRC_NC ? __ldg(p) : __ldcg(p)); };
   auto scalar = [&](int64_t i) {
     float acc = ld1(src[0] + i);
 #pragma unroll
-    for (int k = 1; k < NS_MAX; ++k)
-      if (k < ns) acc = __fadd_rn(acc, ld1(src[k] + i));
+    for (int k = 1; k < NS; ++k) acc = __fadd_rn(acc, ld1(src[k] + i));
     if (SCALE) acc = __fmul_rn(acc, s);
     const T y = E::from_f(acc);
 #pragma unroll
-    for (int j = 0; j < kMaxWorld; ++j)
-      if (j < nd) dst[j][i] = y;
+    for (int j = 0; j < ND; ++j) dst[j][i] = y;
   };
 
   if (mis != 0) {
@@ -128,42 +123,38 @@ __device__ __forceinline__ void cta_xfer(T* const (&dst)[kMaxWorld], int nd,
   if (head > n) head = n;
   for (int64_t i = tid; i < head; i += nt) scalar(i);
   const int64_t nv = (n - head) / VE;
-  auto vec = [&](int64_t v, const uint4 (&in)[NS_MAX]) {
+  auto vec = [&](int64_t v, const uint4 (&in)[NS]) {
     float acc[8], f[8];
     E::unpack(in[0], acc);
 #pragma unroll
-    for (int k = 1; k < NS_MAX; ++k)
-      if (k < ns) {
-        E::unpack(in[k], f);
+    for (int k = 1; k < NS; ++k) {
+      E::unpack(in[k], f);
 #pragma unroll
-        for (int e = 0; e < VE; ++e) acc[e] = __fadd_rn(acc[e], f[e]);
-      }
+      for (int e = 0; e < VE; ++e) acc[e] = __fadd_rn(acc[e], f[e]);
+    }
     if (SCALE) {
 #pragma unroll
       for (int e = 0; e < VE; ++e) acc[e] = __fmul_rn(acc[e], s);
     }
     const uint4 y = E::pack(acc);
 #pragma unroll
-    for (int j = 0; j < kMaxWorld; ++j)
-      if (j < nd) st_v4(dst[j] + head + v * VE, y);
+    for (int j = 0; j < ND; ++j) st_v4(dst[j] + head + v * VE, y);
   };
   auto ldv = [&](const T* p) -> uint4 { return SRC_NC ? ld_nc_v4(p) : ld_cg_v4(p); };
   int64_t v = tid;
   for (; v + (int64_t)(U - 1) * nt < nv; v += (int64_t)U * nt) {
-    uint4 in[U][NS_MAX];
+    uint4 in[U][NS];
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-      for (int k = 0; k < NS_MAX; ++k)
-        if (k < ns) in[u][k] = ldv(src[k] + head + (v + (int64_t)u * nt) * VE);
+      for (int k = 0; k < NS; ++k) in[u][k] = ldv(src[k] + head + (v + (int64_t)u * nt) * VE);
 #pragma unroll
     for (int u = 0; u < U; ++u) vec(v + (int64_t)u * nt, in[u]);
   }
   for (; v < nv; v += nt) {
-    uint4 in[NS_MAX];
+    uint4 in[NS];
 #pragma unroll
-    for (int k = 0; k < NS_MAX; ++k)
-      if (k < ns) in[k] = ldv(src[k] + head + v * VE);
+    for (int k = 0; k < NS; ++k) in[k] = ldv(src[k] + head + v * VE);
     vec(v, in);
   }
   for (int64_t i = head + nv * VE + tid; i < n; i += nt) scalar(i);
@@ -180,43 +171,40 @@ __device__ __forceinline__ int find_slot(const SlotArgs<MAXS>& sa, int64_t x) {
   return a;
 }
 
-// Pack the bucket range [lo, hi) from the gradients into nd buffers:
+// Pack the bucket range [lo, hi) from the gradients into ND buffers:
 // element x goes to dst_j[x - base], scaled by s (Alg. 1, C-2).
-template <typename T, int MAXS>
+template <typename T, int ND, int MAXS>
 __device__ __forceinline__ void walk_pack(const SlotArgs<MAXS>& sa, int64_t lo, int64_t hi,
-                                          T* const (&dstb)[kMaxWorld], int nd, int64_t base,
-                                          float s, int64_t gstride) {
+                                          T* const (&dstb)[ND], int64_t base, float s, int64_t gstride) {
   if (lo >= hi) return;
   for (int k = find_slot(sa, lo); k < sa.n && lo < hi; ++k) {
     const int64_t s0 = sa.off[k], e = min(hi, sa.off[k + 1]);
     if (e <= lo) continue;
     const T* g = reinterpret_cast<const T*>(static_cast<const char*>(sa.grad[k]) + gstride) + (lo - s0);
-    T* d[kMaxWorld];
-    const T* sp[kMaxWorld];
+    T* d[ND];
 #pragma unroll
-    for (int j = 0; j < kMaxWorld; ++j) { d[j] = dstb[j] + (lo - base); sp[j] = g; }
-    cta_xfer<T, 1, true, true>(d, nd, sp, 1, e - lo, s);
+    for (int j = 0; j < ND; ++j) d[j] = dstb[j] + (lo - base);
+    const T* sp[1] = {g};
+    cta_xfer<T, 1, ND, true, true>(d, sp, e - lo, s);
     lo = e;
   }
 }
 
 // Unpack / reduce the bucket range [lo, hi) into the gradients:
-// grad(x) = RNE(sum_k src_k[x - base]) (ns == 1: plain copy back, L246).
-template <typename T, int MAXS>
+// grad(x) = RNE(sum_k src_k[x - base]) (NS == 1: plain copy back).
+template <typename T, int NS, int MAXS>
 __device__ __forceinline__ void walk_unpack(const SlotArgs<MAXS>& sa, int64_t lo, int64_t hi,
-                                            const T* const (&srcb)[kMaxWorld], int ns,
-                                            int64_t base, int64_t gstride) {
+                                            const T* const (&srcb)[NS], int64_t base, int64_t gstride) {
   if (lo >= hi) return;
   for (int k = find_slot(sa, lo); k < sa.n && lo < hi; ++k) {
     const int64_t s0 = sa.off[k], e = min(hi, sa.off[k + 1]);
     if (e <= lo) continue;
     T* g = reinterpret_cast<T*>(static_cast<char*>(sa.grad[k]) + gstride) + (lo - s0);
-    T* d[kMaxWorld];
-    const T* sp[kMaxWorld];
+    T* d[1] = {g};
+    const T* sp[NS];
 #pragma unroll
-    for (int j = 0; j < kMaxWorld; ++j) { d[j] = g; sp[j] = srcb[j] + (lo - base); }
-    if (ns == 1) cta_xfer<T, 1, false, false>(d, 1, sp, 1, e - lo, 1.0f);
-    else cta_xfer<T, kMaxWorld, false, false>(d, 1, sp, ns, e - lo, 1.0f);
+    for (int j = 0; j < NS; ++j) sp[j] = srcb[j] + (lo - base);
+    cta_xfer<T, NS, 1, false, false>(d, sp, e - lo, 1.0f);
     lo = e;
   }
 }

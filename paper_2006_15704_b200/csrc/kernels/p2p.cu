@@ -49,13 +49,17 @@ __device__ __forceinline__ uint32_t* flag_ptr(void* storage, int64_t flags_off, 
   return reinterpret_cast<uint32_t*>(static_cast<char*>(storage) + flags_off) + cta * kMaxWorld + src;
 }
 
+template <int W>
 __device__ __forceinline__ void p2p_barrier(const P2PLaunch& a, int r, uint32_t val) {
-  if (a.world == 1) return;
+  if (W == 1) {  // no peers; the phases still hand data between threads of the CTA
+    __syncthreads();
+    return;
+  }
   __threadfence_system();  // every thread: its remote stores are visible system-wide
   __syncthreads();
   const int t = threadIdx.x;
   const int c = blockIdx.x;
-  if (t < a.world && t != r) {
+  if (t < W && t != r) {
     uint32_t* f = flag_ptr(a.storage[t], a.flags_byte_off, c, r);
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(val) : "memory");
     const uint32_t* mine = flag_ptr(a.storage[r], a.flags_byte_off, c, t);
@@ -78,10 +82,9 @@ __device__ __forceinline__ T* at(void* base, int64_t byte_off) {
   return reinterpret_cast<T*>(static_cast<char*>(base) + byte_off);
 }
 
-template <typename T, int MAXS>
-__global__ void __launch_bounds__(kThreads, 1)
+template <typename T, int W, int MAXS>
+__global__ void __launch_bounds__(kThreads, W <= 2 ? 2 : 1)
     twoshot_kernel(const __grid_constant__ SlotArgs<MAXS> sa, const __grid_constant__ P2PLaunch a) {
-  const int W = a.world;
   const int r = a.emulated ? (int)blockIdx.y : a.rank;
   const int64_t gstride = a.emulated ? (int64_t)r * a.grad_rank_stride : 0;
   const int c = blockIdx.x;
@@ -90,39 +93,40 @@ __global__ void __launch_bounds__(kThreads, 1)
   auto chunk_hi = [&](int j) { return min(j * L + min((int64_t)(c + 1) * a.chunk, L), N); };
 
   // A: pack + scale, push chunk c of shard j into rank j's staging slot r.
+#pragma unroll 1
   for (int i = 1; i <= W; ++i) {
-    const int j = (r + i) % W;  // self last; peers in rotated order
-    T* d[kMaxWorld] = {at<T>(a.storage[j], a.stage_byte_off + (int64_t)r * a.stage_stride)};
-    walk_pack<T, MAXS>(sa, chunk_lo(j), chunk_hi(j), d, 1, j * L, a.scale, gstride);
+    const int j = (r + i) % W;  // peers in rotated order, self last
+    T* d[1] = {at<T>(a.storage[j], a.stage_byte_off + (int64_t)r * a.stage_stride)};
+    walk_pack<T, 1, MAXS>(sa, chunk_lo(j), chunk_hi(j), d, j * L, a.scale, gstride);
   }
-  p2p_barrier(a, r, a.seq);
+  p2p_barrier<W>(a, r, a.seq);
 
-  // C: reduce own shard chunk from the W local slots (rank order), push result
-  // into every rank's bucket (all-gather), starting with the next peer.
+  // C: reduce own shard chunk from the W local slots (rank order), push the
+  // result into every rank's bucket (all-gather), next peer first.
   {
     const int64_t lo = chunk_lo(r), hi = chunk_hi(r);
     if (lo < hi) {
-      const T* src[kMaxWorld];
-      T* dst[kMaxWorld];
+      const T* src[W];
+      T* dst[W];
 #pragma unroll
-      for (int q = 0; q < kMaxWorld; ++q) {
+      for (int q = 0; q < W; ++q) {
         src[q] = at<T>(a.storage[r], a.stage_byte_off + (int64_t)q * a.stage_stride) + (lo - r * L);
         dst[q] = at<T>(a.storage[(r + 1 + q) % W], a.bucket_byte_off) + lo;
       }
-      cta_xfer<T, kMaxWorld, false, false>(dst, W, src, W, hi - lo, 1.0f);
+      cta_xfer<T, W, W, false, false>(dst, src, hi - lo, 1.0f);
     }
   }
-  p2p_barrier(a, r, a.seq + 1);
+  p2p_barrier<W>(a, r, a.seq + 1);
 
   // E: unpack every shard's chunk c from the local bucket into the gradients.
-  const T* b[kMaxWorld] = {at<T>(a.storage[r], a.bucket_byte_off)};
-  for (int j = 0; j < W; ++j) walk_unpack<T, MAXS>(sa, chunk_lo(j), chunk_hi(j), b, 1, 0, gstride);
+  const T* b[1] = {at<T>(a.storage[r], a.bucket_byte_off)};
+#pragma unroll 1
+  for (int j = 0; j < W; ++j) walk_unpack<T, 1, MAXS>(sa, chunk_lo(j), chunk_hi(j), b, 0, gstride);
 }
 
-template <typename T, int MAXS>
-__global__ void __launch_bounds__(kThreads, 1)
+template <typename T, int W, int MAXS>
+__global__ void __launch_bounds__(kThreads, W <= 2 ? 2 : 1)
     oneshot_kernel(const __grid_constant__ SlotArgs<MAXS> sa, const __grid_constant__ P2PLaunch a) {
-  const int W = a.world;
   const int r = a.emulated ? (int)blockIdx.y : a.rank;
   const int64_t gstride = a.emulated ? (int64_t)r * a.grad_rank_stride : 0;
   const int64_t lo = min((int64_t)blockIdx.x * a.chunk, a.numel);
@@ -130,20 +134,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // A: pack + scale once, push to slot r of every rank (self included).
   {
-    T* d[kMaxWorld];
+    T* d[W];
 #pragma unroll
-    for (int q = 0; q < kMaxWorld; ++q)
+    for (int q = 0; q < W; ++q)
       d[q] = at<T>(a.storage[(r + 1 + q) % W], a.stage_byte_off + (int64_t)r * a.stage_stride);
-    walk_pack<T, MAXS>(sa, lo, hi, d, W, 0, a.scale, gstride);
+    walk_pack<T, W, MAXS>(sa, lo, hi, d, 0, a.scale, gstride);
   }
-  p2p_barrier(a, r, a.seq);
+  p2p_barrier<W>(a, r, a.seq);
 
   // C: reduce the W local slots in rank order straight into the gradients.
-  const T* s[kMaxWorld];
+  const T* s[W];
 #pragma unroll
-  for (int q = 0; q < kMaxWorld; ++q)
-    s[q] = at<T>(a.storage[r], a.stage_byte_off + (int64_t)q * a.stage_stride);
-  walk_unpack<T, MAXS>(sa, lo, hi, s, W, 0, gstride);
+  for (int q = 0; q < W; ++q) s[q] = at<T>(a.storage[r], a.stage_byte_off + (int64_t)q * a.stage_stride);
+  walk_unpack<T, W, MAXS>(sa, lo, hi, s, 0, gstride);
 }
 
 template <int MAXS>
@@ -159,9 +162,23 @@ SlotArgs<MAXS> make_args(const SlotView& sv) {
 }
 
 template <typename T, int MAXS>
-void* kernel_ptr(int algo) {
-  return algo == 3 ? reinterpret_cast<void*>(twoshot_kernel<T, MAXS>)
-                   : reinterpret_cast<void*>(oneshot_kernel<T, MAXS>);
+void* kernel_ptr(int algo, int world) {
+#define B200DDP_K(WW)                                                      \
+  case WW:                                                                 \
+    return algo == 3 ? reinterpret_cast<void*>(twoshot_kernel<T, WW, MAXS>) \
+                     : reinterpret_cast<void*>(oneshot_kernel<T, WW, MAXS>);
+  switch (world) {
+    B200DDP_K(1) B200DDP_K(2) B200DDP_K(3) B200DDP_K(4) B200DDP_K(5) B200DDP_K(6) B200DDP_K(7) B200DDP_K(8)
+    default: return nullptr;
+  }
+#undef B200DDP_K
+}
+
+template <typename T>
+void* kernel_for(int algo, int world, int n_slots) {
+  if (n_slots <= 32) return kernel_ptr<T, 32>(algo, world);
+  if (n_slots <= 256) return kernel_ptr<T, 256>(algo, world);
+  return kernel_ptr<T, 1024>(algo, world);
 }
 
 template <typename T, int MAXS>
@@ -169,7 +186,8 @@ cudaError_t run(int algo, const SlotView& sv, const P2PLaunch& a, cudaStream_t s
   const SlotArgs<MAXS> sargs = make_args<MAXS>(sv);
   P2PLaunch pa = a;
   void* args[] = {const_cast<SlotArgs<MAXS>*>(&sargs), &pa};
-  void* fn = kernel_ptr<T, MAXS>(algo);
+  void* fn = kernel_ptr<T, MAXS>(algo, a.world);
+  if (!fn) return cudaErrorInvalidValue;
   if (a.emulated) {
     return cudaLaunchCooperativeKernel(fn, dim3(a.ctas, a.world), dim3(kThreads), args, 0, st);
   }
@@ -178,21 +196,17 @@ cudaError_t run(int algo, const SlotView& sv, const P2PLaunch& a, cudaStream_t s
 
 template <typename T>
 cudaError_t dispatch(int algo, const SlotView& sv, const P2PLaunch& a, cudaStream_t st) {
-  if (sv.n <= 16) return run<T, 16>(algo, sv, a, st);
-  if (sv.n <= 64) return run<T, 64>(algo, sv, a, st);
+  if (sv.n <= 32) return run<T, 32>(algo, sv, a, st);
   if (sv.n <= 256) return run<T, 256>(algo, sv, a, st);
   if (sv.n <= kMaxSlotsPerLaunch) return run<T, 1024>(algo, sv, a, st);
   return cudaErrorInvalidValue;
 }
 
 template <typename T>
-int occupancy(int algo, int n_slots) {
+int occupancy(int algo, int world, int n_slots) {
   int blocks = 0;
-  void* fn = n_slots <= 16    ? kernel_ptr<T, 16>(algo)
-             : n_slots <= 64  ? kernel_ptr<T, 64>(algo)
-             : n_slots <= 256 ? kernel_ptr<T, 256>(algo)
-                              : kernel_ptr<T, 1024>(algo);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kThreads, 0) != cudaSuccess) return 0;
+  void* fn = kernel_for<T>(algo, world, n_slots);
+  if (!fn || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kThreads, 0) != cudaSuccess) return 0;
   return blocks;
 }
 
@@ -206,7 +220,8 @@ int emulated_max_ctas(int algo, int dtype, int n_slots, int world) {
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
-  const int occ = dtype == 0 ? occupancy<float>(algo, n_slots) : occupancy<__nv_bfloat16>(algo, n_slots);
+  const int occ = dtype == 0 ? occupancy<float>(algo, world, n_slots)
+                             : occupancy<__nv_bfloat16>(algo, world, n_slots);
   return occ * sms / (world > 0 ? world : 1);
 }
 

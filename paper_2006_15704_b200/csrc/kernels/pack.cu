@@ -24,9 +24,9 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ 
                                                         T* __restrict__ bucket, float s) {
   constexpr int64_t tile = kTileBytes / sizeof(T);
   const int64_t lo0 = sa.off[0], hi0 = sa.off[sa.n];
-  T* d[kMaxWorld] = {bucket};
+  T* d[1] = {bucket};
   for (int64_t t = lo0 + (int64_t)blockIdx.x * tile; t < hi0; t += (int64_t)gridDim.x * tile)
-    walk_pack<T, MAXS>(sa, t, min(t + tile, hi0), d, 1, 0, s, 0);
+    walk_pack<T, 1, MAXS>(sa, t, min(t + tile, hi0), d, 0, s, 0);
 }
 
 template <typename T, int MAXS>
@@ -34,9 +34,9 @@ __global__ void __launch_bounds__(kThreads) unpack_kernel(const __grid_constant_
                                                           const T* __restrict__ bucket) {
   constexpr int64_t tile = kTileBytes / sizeof(T);
   const int64_t lo0 = sa.off[0], hi0 = sa.off[sa.n];
-  const T* src[kMaxWorld] = {bucket};
+  const T* src[1] = {bucket};
   for (int64_t t = lo0 + (int64_t)blockIdx.x * tile; t < hi0; t += (int64_t)gridDim.x * tile)
-    walk_unpack<T, MAXS>(sa, t, min(t + tile, hi0), src, 1, 0, 0);
+    walk_unpack<T, 1, MAXS>(sa, t, min(t + tile, hi0), src, 0, 0);
 }
 
 template <int MAXS>
