@@ -14,7 +14,7 @@ ddp_finalize_backward closes the pass.  With no backward compute to hide
 behind, the whole sync is exposed: `value` = device ms per step (CUDA events
 on the producer stream, max over ranks), lower is better.  `busbw` reports the
 bucket allreduce bus bandwidth of a 25 MiB bucket (N > 1).  L2 (126 MB) is
-flushed between timed steps by a 256 MiB memset outside the per-step events.
+flushed between timed steps (256 MiB written then read) outside the per-step events.
 
 For N > 1 launch with torchrun (one process per GPU); rank 0 prints ONE JSON
 line.  `--impl reference` times the oracle (oracle/, numpy on host cores) on
@@ -188,7 +188,13 @@ def run_ours(a):
     sdev.fill_all(grads, 15704, rank, 0, "normal", a.dtype)
     order = list(range(len(ns) - 1, -1, -1))
     batch = L.ReadyBatch(order, [grads[p].data_ptr() for p in order])
-    flush = torch.empty(256 * MIB, dtype=torch.uint8, device=dev)
+    flush = torch.zeros(256 * MIB // 8, dtype=torch.int64, device=dev)
+
+    def flush_l2():
+        # write then read 256 MiB (> 126 MB L2): evicts the step's data and leaves
+        # clean lines, so no dirty write-back is charged to the next step
+        flush.add_(1)
+        flush.sum()
     stream = torch.cuda.current_stream(dev)
 
     def step():
@@ -203,7 +209,7 @@ def run_ours(a):
     def timed(fn, k, pre=None):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
         for i in range(k):
-            flush.zero_()
+            flush_l2()
             if pre:
                 pre()
             evs[i][0].record(stream)
@@ -337,7 +343,7 @@ def run_ours(a):
             "data": "synthetic (seeded splitmix64 gradients shaped like the workload; no model compute)",
             "config": {"workload": workload_name(a), "params": sum(ns), "tensors": len(ns),
                        "buckets": len(bnumel), "bucket_algos": algos, "bucket_cap_mib": a.cap_mib,
-                       "grad_bytes_per_step": S_tot, "l2": "flushed between steps (256 MiB memset outside events)",
+                       "grad_bytes_per_step": S_tot, "l2": "flushed between steps (256 MiB write + read, outside the per-step events)",
                        "ready_order": "reverse registration, one batched ddp_grads_ready per step",
                        "parallelism": f"dp{world}"},
             "busbw": busbw,
