@@ -247,7 +247,7 @@ def run_ours(a):
     S_tot = sum(bnumel) * esize
     launches_per_step = sum(1 if x != "nccl" else 2 for x in algos)
 
-    # dominant kernel roofline
+    # dominant kernel roofline: algorithmic bytes per launch / measured launch time
     peak_hbm, peak_src = measured_peaks()
     kinds = {k: v for k, v in prof.items() if v[1] > 0}
     dom = max(kinds, key=lambda k: kinds[k][0]) if kinds else None
@@ -255,23 +255,28 @@ def run_ours(a):
     if dom is not None:
         tot_ms, cnt = kinds[dom]
         avg_ms = tot_ms / cnt
-        n_p2p = sum(1 for x in algos if x != "nccl")
+        p2p = [(n * esize, x) for n, x in zip(bnumel, algos) if x != "nccl"]
+        ncl = [n * esize for n, x in zip(bnumel, algos) if x == "nccl"]
         if dom == "p2p_fused" and world == 1:
-            # W=1 fused one-shot: pack (2S) + unpack (2S) of every P2P bucket
-            byts = 4 * sum(n * esize for n, x in zip(bnumel, algos) if x != "nccl") / max(1, n_p2p)
-            roof = {"bound": "hbm", "achieved": byts / (avg_ms * 1e-3) / 1e9, "peak": peak_hbm, "unit": "GB/s"}
+            # world 1 fused kernel: read grad S, write bucket S, write grad S (3 S per bucket)
+            byts, bound, per = 3 * sum(b for b, _ in p2p) / len(p2p), "hbm", "3 x bucket bytes"
         elif dom in ("pack", "unpack"):
-            byts = 2 * sum(n * esize for n, x in zip(bnumel, algos) if x == "nccl") / max(1, len(algos) - n_p2p)
-            roof = {"bound": "hbm", "achieved": byts / (avg_ms * 1e-3) / 1e9, "peak": peak_hbm, "unit": "GB/s"}
+            byts, bound, per = 2 * sum(ncl) / len(ncl), "hbm", "2 x bucket bytes"
+        elif dom == "p2p_fused":
+            # NVLink bytes sent per GPU per direction: one-shot (W-1) S, two-shot 2 (W-1)/W S
+            byts = sum(b * ((world - 1) if x == "oneshot" else 2 * (world - 1) / world) for b, x in p2p) / len(p2p)
+            bound, per = "nvlink", "NVLink bytes per direction: one-shot (W-1)S, two-shot 2(W-1)/W S"
         else:
-            # NVLink bound: 2(W-1)/W * S bytes per direction per GPU (ring / two-shot)
-            sel = [n * esize for n, x in zip(bnumel, algos) if (x == "nccl") == (dom == "nccl_allreduce")]
-            byts = 2 * (world - 1) / world * sum(sel) / max(1, len(sel))
-            roof = {"bound": "nvlink", "achieved": byts / (avg_ms * 1e-3) / 1e9, "peak": 770.0, "unit": "GB/s"}
+            byts, bound, per = 2 * (world - 1) / world * sum(ncl) / len(ncl), "nvlink", "2(W-1)/W x bucket bytes"
+        peak = peak_hbm if bound == "hbm" else 770.0
+        roof = {"bound": bound, "achieved": byts / (avg_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s"}
         roof["frac"] = roof["achieved"] / roof["peak"]
         roof["traffic"] = None
         roof["kernel"] = dom
-        roof["peak_source"] = peak_src if roof["bound"] == "hbm" else "B200_PROFILING.md peer copy 770 GB/s/dir"
+        roof["algorithmic_bytes_per_launch"] = byts
+        roof["bytes_rule"] = per
+        roof["peak_source"] = (f"MEASURED_PEAKS.json hbm_gbs ({peak_src})" if bound == "hbm"
+                               else "B200_PROFILING.md measured peer copy 770 GB/s per direction")
         roof["avg_launch_ms"] = avg_ms
 
     # ---- bucket allreduce bus bandwidth on a 25 MiB bucket (N > 1) ------------------

@@ -39,6 +39,7 @@ int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 constexpr int64_t kMinChunkElems = 4096;   // smallest per-CTA chunk worth a CTA
+constexpr int64_t kSubElemBytes = 32 * 1024; // pipeline stage per CTA (one 16-B vector x 4 per thread)
 constexpr int64_t kBarrierScratch = 32 * 1024;  // scratch int inside the flags region
 
 struct Bucket {
@@ -49,7 +50,8 @@ struct Bucket {
   int64_t byte_off = 0;         // inside the symmetric storage
   int algo = DDP_ALGO_NCCL;
   int ctas = 1;
-  int64_t shard = 0, chunk = 0;
+  int64_t shard = 0, chunk = 0, sub = 0;
+  int32_t stages = 0;
 };
 
 enum class State { CREATED, IDLE, IN_PASS };
@@ -178,6 +180,8 @@ void grid_for(const ddp_ctx* c, Bucket& bk, int max_ctas) {
   bk.shard = L;
   bk.chunk = Q;
   bk.ctas = (int)C;
+  bk.sub = std::min<int64_t>(Q, kSubElemBytes / c->esize);
+  bk.stages = (int32_t)cdiv(Q, bk.sub);
 }
 
 int max_ctas_for(const ddp_ctx* c, const Bucket& bk) {
@@ -281,11 +285,13 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   a.rank = c->rank;
   a.ctas = bk.ctas;
   a.emulated = c->emulated ? 1 : 0;
+  a.sub = bk.sub;
+  a.stages = bk.stages;
   a.seq = c->p2p_seq;
   a.scale = scale;
   a.grad_rank_stride = c->grad_rank_stride;
   a.err = c->err_dev;
-  c->p2p_seq += 2;
+  c->p2p_seq += (uint32_t)bk.stages + 2;  // flag values used: seq .. seq + stages + 1
   c->p2p_launches += 1;
   prof_begin(c, 3);
   CUDA_TRY(c, launch_p2p(bk.algo, c->dtype, sv, a, c->comm));

@@ -9,7 +9,8 @@ namespace b200ddp {
 
 constexpr int kMaxWorld = 8;
 constexpr int kMaxCtas = 256;                  // rows of the barrier flag table
-constexpr int64_t kFlagsBytes = 64 * 1024;     // >= kMaxCtas * kMaxWorld * 4, 64 KiB aligned
+constexpr int64_t kFlagsBytes = 64 * 1024;     // 2 flag arrays of kMaxCtas * kMaxWorld uint32 + scratch
+constexpr int64_t kFlagArrayBytes = kMaxCtas * kMaxWorld * 4;
 constexpr int kMaxSlotsPerLaunch = 1024;       // largest by-value slot table
 constexpr int64_t kAlignElems = 256;           // shard / chunk granularity (elements)
 constexpr int kThreads = 512;                  // threads per CTA for every kernel
@@ -24,13 +25,15 @@ struct SlotView {
 // Per-launch description of a P2P allreduce (one-shot or two-shot).
 struct P2PLaunch {
   void* storage[kMaxWorld];   // every rank's symmetric storage base (peer-mapped)
-  int64_t flags_byte_off;     // barrier flags: uint32 [kMaxCtas][kMaxWorld], [cta][src rank]
+  int64_t flags_byte_off;     // flags: uint32 [2][kMaxCtas][kMaxWorld] = [stage kind][cta][src rank]
   int64_t bucket_byte_off;    // this bucket inside the bucket region
   int64_t stage_byte_off;     // staging region for this launch (parity applied)
   int64_t stage_stride;       // bytes between per-source staging slots
   int64_t numel;              // bucket elements
   int64_t shard;              // two-shot shard length L (elements); unused by one-shot
   int64_t chunk;              // per-CTA chunk Q (elements)
+  int64_t sub;                // pipeline sub-chunk (elements); stages = ceil(chunk / sub)
+  int32_t stages;
   int32_t world;
   int32_t rank;               // this rank (ignored when emulated: rank = blockIdx.y)
   int32_t ctas;               // gridDim.x

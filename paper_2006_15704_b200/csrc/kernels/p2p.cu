@@ -45,24 +45,34 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-__device__ __forceinline__ uint32_t* flag_ptr(void* storage, int64_t flags_off, int cta, int src) {
-  return reinterpret_cast<uint32_t*>(static_cast<char*>(storage) + flags_off) + cta * kMaxWorld + src;
+// flags: uint32 [2][kMaxCtas][kMaxWorld]; kind 0 = "pushed (reduce-scatter /
+// one-shot data) through stage k", kind 1 = "all-gather pushed through stage k".
+__device__ __forceinline__ uint32_t* flag_ptr(void* storage, int64_t flags_off, int kind, int cta, int src) {
+  return reinterpret_cast<uint32_t*>(static_cast<char*>(storage) + flags_off + kind * kFlagArrayBytes) +
+         cta * kMaxWorld + src;
 }
 
+// Publish "this CTA's stores up to here are done" to the same CTA index of every
+// peer: all threads fence their (remote) stores at system scope, then one thread
+// per peer writes the monotonic value with release semantics.
 template <int W>
-__device__ __forceinline__ void p2p_barrier(const P2PLaunch& a, int r, uint32_t val) {
-  if (W == 1) {  // no peers; the phases still hand data between threads of the CTA
-    __syncthreads();
-    return;
-  }
-  __threadfence_system();  // every thread: its remote stores are visible system-wide
+__device__ __forceinline__ void p2p_signal(const P2PLaunch& a, int r, int kind, uint32_t val) {
+  if (W == 1) return;
+  __threadfence_system();
   __syncthreads();
   const int t = threadIdx.x;
-  const int c = blockIdx.x;
   if (t < W && t != r) {
-    uint32_t* f = flag_ptr(a.storage[t], a.flags_byte_off, c, r);
+    uint32_t* f = flag_ptr(a.storage[t], a.flags_byte_off, kind, blockIdx.x, r);
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(val) : "memory");
-    const uint32_t* mine = flag_ptr(a.storage[r], a.flags_byte_off, c, t);
+  }
+}
+
+// Wait until every peer's same-index CTA has published >= val (bounded spin).
+template <int W>
+__device__ __forceinline__ void p2p_wait(const P2PLaunch& a, int r, int kind, uint32_t val) {
+  const int t = threadIdx.x;
+  if (W > 1 && t < W && t != r) {
+    const uint32_t* mine = flag_ptr(a.storage[r], a.flags_byte_off, kind, blockIdx.x, t);
     const uint64_t t0 = globaltimer();
     while (true) {
       uint32_t v;
@@ -82,71 +92,128 @@ __device__ __forceinline__ T* at(void* base, int64_t byte_off) {
   return reinterpret_cast<T*>(static_cast<char*>(base) + byte_off);
 }
 
+// Two-shot, software-pipelined over `stages` sub-chunks of the CTA's chunk:
+// iteration k pushes reduce-scatter data of stage k, reduces + all-gathers
+// stage k-1 and unpacks stage k-2, so NVLink stores of one stage overlap the
+// local reduction / unpack of the previous ones.
 template <typename T, int W, int MAXS>
 __global__ void __launch_bounds__(kThreads, W <= 2 ? 2 : 1)
     twoshot_kernel(const __grid_constant__ SlotArgs<MAXS> sa, const __grid_constant__ P2PLaunch a) {
   const int r = a.emulated ? (int)blockIdx.y : a.rank;
   const int64_t gstride = a.emulated ? (int64_t)r * a.grad_rank_stride : 0;
   const int c = blockIdx.x;
-  const int64_t L = a.shard, N = a.numel;
-  auto chunk_lo = [&](int j) { return min(j * L + min((int64_t)c * a.chunk, L), N); };
-  auto chunk_hi = [&](int j) { return min(j * L + min((int64_t)(c + 1) * a.chunk, L), N); };
+  const int64_t L = a.shard, N = a.numel, Q = a.chunk, SUB = a.sub;
+  const int K = a.stages;
+  // stage k of chunk c of shard j: [j*L + c*Q + k*SUB, ...) clipped to the chunk, shard and bucket
+  auto rng = [&](int j, int k, int64_t& lo, int64_t& hi) {
+    const int64_t c0 = (int64_t)c * Q, c1 = min(c0 + Q, L);
+    lo = min(j * L + min(c0 + (int64_t)k * SUB, c1), N);
+    hi = min(j * L + min(c0 + (int64_t)(k + 1) * SUB, c1), N);
+  };
 
-  // A: pack + scale, push chunk c of shard j into rank j's staging slot r.
 #pragma unroll 1
-  for (int i = 1; i <= W; ++i) {
-    const int j = (r + i) % W;  // peers in rotated order, self last
-    T* d[1] = {at<T>(a.storage[j], a.stage_byte_off + (int64_t)r * a.stage_stride)};
-    walk_pack<T, 1, MAXS>(sa, chunk_lo(j), chunk_hi(j), d, j * L, a.scale, gstride);
-  }
-  p2p_barrier<W>(a, r, a.seq);
-
-  // C: reduce own shard chunk from the W local slots (rank order), push the
-  // result into every rank's bucket (all-gather), next peer first.
-  {
-    const int64_t lo = chunk_lo(r), hi = chunk_hi(r);
-    if (lo < hi) {
-      const T* src[W];
-      T* dst[W];
+  for (int k = 0; k <= K + 1; ++k) {
+    if (k < K) {  // A: pack + scale, push stage k of every shard j into rank j's slot r
 #pragma unroll
-      for (int q = 0; q < W; ++q) {
-        src[q] = at<T>(a.storage[r], a.stage_byte_off + (int64_t)q * a.stage_stride) + (lo - r * L);
-        dst[q] = at<T>(a.storage[(r + 1 + q) % W], a.bucket_byte_off) + lo;
+      for (int i = 1; i <= W; ++i) {
+        const int j = (r + i) % W;  // peers in rotated order, self last
+        int64_t lo, hi;
+        rng(j, k, lo, hi);
+        if (lo >= hi) continue;
+        T* d[1] = {at<T>(a.storage[j], a.stage_byte_off + (int64_t)r * a.stage_stride)};
+        walk_pack<T, 1, MAXS>(sa, lo, hi, d, j * L, a.scale, gstride);
       }
-      cta_xfer<T, W, W, false, false>(dst, src, hi - lo, 1.0f);
+    }
+    if (k >= 1 && k <= K) {  // C: reduce own shard, stage k-1; all-gather into every bucket
+      p2p_wait<W>(a, r, 0, a.seq + (uint32_t)k);
+      int64_t lo, hi;
+      rng(r, k - 1, lo, hi);
+      if (lo < hi) {
+        const T* src[W];
+        T* dst[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          src[q] = at<T>(a.storage[r], a.stage_byte_off + (int64_t)q * a.stage_stride) + (lo - r * L);
+          dst[q] = at<T>(a.storage[(r + 1 + q) % W], a.bucket_byte_off) + lo;
+        }
+        cta_xfer<T, W, W, false, false>(dst, src, hi - lo, 1.0f);
+      }
+    }
+    if (k >= 2) {  // E: unpack stage k-2 of every shard from the local bucket
+      p2p_wait<W>(a, r, 1, a.seq + (uint32_t)(k - 1));
+      const T* b[1] = {at<T>(a.storage[r], a.bucket_byte_off)};
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        int64_t lo, hi;
+        rng(j, k - 2, lo, hi);
+        if (lo < hi) walk_unpack<T, 1, MAXS>(sa, lo, hi, b, 0, gstride);
+      }
+    }
+    if (W == 1) {
+      __syncthreads();
+    } else if (k <= K) {
+      p2p_signal<W>(a, r, 0, a.seq + (uint32_t)(k + 1));  // through stage k (k == K: harmless)
+      if (k >= 1) {
+        const int t = threadIdx.x;  // all-gather of stage k-1 is covered by the same fence
+        if (t < W && t != r) {
+          uint32_t* f = flag_ptr(a.storage[t], a.flags_byte_off, 1, blockIdx.x, r);
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(a.seq + (uint32_t)k) : "memory");
+        }
+      }
     }
   }
-  p2p_barrier<W>(a, r, a.seq + 1);
-
-  // E: unpack every shard's chunk c from the local bucket into the gradients.
-  const T* b[1] = {at<T>(a.storage[r], a.bucket_byte_off)};
-#pragma unroll 1
-  for (int j = 0; j < W; ++j) walk_unpack<T, 1, MAXS>(sa, chunk_lo(j), chunk_hi(j), b, 0, gstride);
 }
 
+// One-shot, software-pipelined: iteration k pushes stage k of the chunk to
+// slot r of every rank and reduces stage k-1 (W local slots, rank order)
+// straight into the gradients.  Staging is double-buffered by launch parity.
 template <typename T, int W, int MAXS>
 __global__ void __launch_bounds__(kThreads, W <= 2 ? 2 : 1)
     oneshot_kernel(const __grid_constant__ SlotArgs<MAXS> sa, const __grid_constant__ P2PLaunch a) {
   const int r = a.emulated ? (int)blockIdx.y : a.rank;
   const int64_t gstride = a.emulated ? (int64_t)r * a.grad_rank_stride : 0;
-  const int64_t lo = min((int64_t)blockIdx.x * a.chunk, a.numel);
-  const int64_t hi = min(lo + a.chunk, a.numel);
+  const int64_t lo0 = min((int64_t)blockIdx.x * a.chunk, a.numel);
+  const int64_t hi0 = min(lo0 + a.chunk, a.numel);
 
-  // A: pack + scale once, push to slot r of every rank (self included).
-  {
-    T* d[W];
-#pragma unroll
-    for (int q = 0; q < W; ++q)
-      d[q] = at<T>(a.storage[(r + 1 + q) % W], a.stage_byte_off + (int64_t)r * a.stage_stride);
-    walk_pack<T, W, MAXS>(sa, lo, hi, d, 0, a.scale, gstride);
+  if (W == 1) {
+    // A world of one: the allreduce of the packed value s = RNE(g * 1) is s
+    // itself, so each thread packs into the bucket and writes the reduced
+    // value back to .grad from registers (pack, 1-rank reduce, unpack fused).
+    T* st = at<T>(a.storage[r], a.stage_byte_off);
+    for (int k = find_slot(sa, lo0); k < sa.n; ++k) {
+      const int64_t s0 = sa.off[k];
+      if (s0 >= hi0) break;
+      const int64_t x0 = max(lo0, s0), x1 = min(hi0, sa.off[k + 1]);
+      if (x0 >= x1) continue;
+      T* g = reinterpret_cast<T*>(static_cast<char*>(sa.grad[k]) + gstride) + (x0 - s0);
+      T* dd[2] = {st + x0, g};
+      const T* sp[1] = {g};
+      cta_xfer<T, 1, 2, true, true>(dd, sp, x1 - x0, a.scale);
+    }
+    return;
   }
-  p2p_barrier<W>(a, r, a.seq);
 
-  // C: reduce the W local slots in rank order straight into the gradients.
+  const int K = a.stages;
+  T* d[W];
   const T* s[W];
 #pragma unroll
-  for (int q = 0; q < W; ++q) s[q] = at<T>(a.storage[r], a.stage_byte_off + (int64_t)q * a.stage_stride);
-  walk_unpack<T, W, MAXS>(sa, lo, hi, s, 0, gstride);
+  for (int q = 0; q < W; ++q) {
+    d[q] = at<T>(a.storage[(r + 1 + q) % W], a.stage_byte_off + (int64_t)r * a.stage_stride);
+    s[q] = at<T>(a.storage[r], a.stage_byte_off + (int64_t)q * a.stage_stride);
+  }
+#pragma unroll 1
+  for (int k = 0; k <= K; ++k) {
+    if (k < K) {  // A: pack + scale stage k once, push to slot r of every rank
+      const int64_t lo = min(lo0 + (int64_t)k * a.sub, hi0), hi = min(lo + a.sub, hi0);
+      walk_pack<T, W, MAXS>(sa, lo, hi, d, 0, a.scale, gstride);
+    }
+    if (k >= 1) {  // C: stage k-1 from every rank -> reduce in rank order -> .grad
+      p2p_wait<W>(a, r, 0, a.seq + (uint32_t)k);
+      const int64_t lo = min(lo0 + (int64_t)(k - 1) * a.sub, hi0), hi = min(lo + a.sub, hi0);
+      walk_unpack<T, W, MAXS>(sa, lo, hi, s, 0, gstride);
+    }
+    if (k < K) p2p_signal<W>(a, r, 0, a.seq + (uint32_t)(k + 1));
+  }
 }
 
 template <int MAXS>
