@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--algo", type=int, default=0, help="force DDP_OPT_ALGO (0 auto)")
     ap.add_argument("--comm-ctas", type=int, default=0)
     ap.add_argument("--pack-ctas", type=int, default=0)
+    ap.add_argument("--stage-kib", type=int, default=0)
     ap.add_argument("--oneshot-max", type=int, default=-1)
     ap.add_argument("--twoshot-max", type=int, default=-1)
     return ap.parse_args()
@@ -172,6 +173,8 @@ def run_ours(a):
         opts[L.OPT_COMM_CTAS] = a.comm_ctas
     if a.pack_ctas:
         opts[L.OPT_PACK_CTAS] = a.pack_ctas
+    if a.stage_kib:
+        opts[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
     if a.oneshot_max >= 0:
         opts[L.OPT_P2P_ONESHOT_MAX] = a.oneshot_max
     if a.twoshot_max >= 0:

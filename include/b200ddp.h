@@ -74,7 +74,9 @@ enum {
   DDP_OPT_DRY_RUN = 5,          /* 1: protocol only, no device work (host tests; CREATED only) */
   DDP_OPT_PROFILE = 6,          /* 1: time every device launch with CUDA events */
   DDP_OPT_ALGO = 7,             /* force the bucket allreduce: 0 auto, 1 NCCL, 2 one-shot, 3 two-shot */
-  DDP_OPT_PACK_CTAS = 8         /* max CTAs of pack/unpack kernels and of P2P kernels at world 1 */
+  DDP_OPT_PACK_CTAS = 8,        /* max CTAs of pack/unpack kernels and of P2P kernels at world 1 */
+  DDP_OPT_P2P_STAGE_BYTES = 9   /* 0 (default): one pipeline stage per CTA chunk; else split each
+                                   CTA chunk into stages of this many bytes (one sync per stage) */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO. */

@@ -23,7 +23,7 @@ STATUS_NAMES = ["OK", "INVALID_ARG", "STATE", "DUPLICATE", "INCOMPLETE", "CUDA",
                 "POISONED", "TIMEOUT", "UNSUPPORTED"]
 FP32, BF16 = 0, 1
 OPT_OVERLAP, OPT_P2P_ONESHOT_MAX, OPT_P2P_TWOSHOT_MAX, OPT_COMM_CTAS, OPT_DRY_RUN, OPT_PROFILE, \
-    OPT_ALGO, OPT_PACK_CTAS = range(1, 9)
+    OPT_ALGO, OPT_PACK_CTAS, OPT_P2P_STAGE_BYTES = range(1, 10)
 ALGO_AUTO, ALGO_NCCL, ALGO_ONESHOT, ALGO_TWOSHOT = range(4)
 ALGO_NAMES = {ALGO_NCCL: "nccl", ALGO_ONESHOT: "oneshot", ALGO_TWOSHOT: "twoshot"}
 PROFILE_KINDS = ("pack", "nccl_allreduce", "unpack", "p2p_fused")

@@ -39,7 +39,10 @@ int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 constexpr int64_t kMinChunkElems = 4096;   // smallest per-CTA chunk worth a CTA
-constexpr int64_t kSubElemBytes = 32 * 1024; // pipeline stage per CTA (one 16-B vector x 4 per thread)
+// Pipeline stage per CTA.  A cross-GPU sync point costs ~4-8 us of fence plus
+// ~3 us of flag flight (tools/sync_probe.cu on B200), so the default is one
+// stage per chunk (one sync for one-shot, two for two-shot); DDP_OPT_P2P_STAGE_BYTES
+// splits chunks for experiments.
 constexpr int64_t kBarrierScratch = 32 * 1024;  // scratch int inside the flags region
 
 struct Bucket {
@@ -73,7 +76,7 @@ struct ddp_ctx {
   std::vector<int64_t> p_off;
   // options
   int64_t overlap = 1, oneshot_max = 256 * 1024, twoshot_max = INT64_MAX, comm_ctas = 32,
-          dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 2;
+          dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 2, stage_bytes = 0;
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
           stage1_stride = 0, storage_bytes = 0;
@@ -180,7 +183,7 @@ void grid_for(const ddp_ctx* c, Bucket& bk, int max_ctas) {
   bk.shard = L;
   bk.chunk = Q;
   bk.ctas = (int)C;
-  bk.sub = std::min<int64_t>(Q, kSubElemBytes / c->esize);
+  bk.sub = c->stage_bytes > 0 ? std::max<int64_t>(kAlignElems, std::min<int64_t>(Q, c->stage_bytes / c->esize)) : Q;
   bk.stages = (int32_t)cdiv(Q, bk.sub);
 }
 
@@ -622,6 +625,11 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       c->pack_ctas = v;
       regrid(c);
       return DDP_OK;
+    case DDP_OPT_P2P_STAGE_BYTES:
+      if (v < 0) return fail(DDP_ERR_INVALID_ARG, "negative stage bytes");
+      c->stage_bytes = v;
+      regrid(c);
+      return DDP_OK;
     default:
       return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
@@ -640,6 +648,7 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_PROFILE: *v = c->profile; break;
     case DDP_OPT_ALGO: *v = c->algo; break;
     case DDP_OPT_PACK_CTAS: *v = c->pack_ctas; break;
+    case DDP_OPT_P2P_STAGE_BYTES: *v = c->stage_bytes; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;

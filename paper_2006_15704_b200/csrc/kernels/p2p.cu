@@ -53,15 +53,17 @@ __device__ __forceinline__ uint32_t* flag_ptr(void* storage, int64_t flags_off, 
 }
 
 // Publish "this CTA's stores up to here are done" to the same CTA index of every
-// peer: all threads fence their (remote) stores at system scope, then one thread
-// per peer writes the monotonic value with release semantics.
+// peer.  bar.sync orders every thread's stores before the signalling threads
+// (CTA-scope synchronization, cumulative); each signalling thread then fences
+// at system scope and writes the monotonic value with release semantics.  Only
+// W-1 threads of warp 0 fence: a MEMBAR.SYS per warp of the CTA would serialize.
 template <int W>
 __device__ __forceinline__ void p2p_signal(const P2PLaunch& a, int r, int kind, uint32_t val) {
   if (W == 1) return;
-  __threadfence_system();
   __syncthreads();
   const int t = threadIdx.x;
   if (t < W && t != r) {
+    __threadfence_system();
     uint32_t* f = flag_ptr(a.storage[t], a.flags_byte_off, kind, blockIdx.x, r);
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(val) : "memory");
   }

@@ -86,9 +86,11 @@ def test_knobs_never_change_values():
     ns = numels("resnet50")[:40]
     W = 4
     base = None
-    for cap, algo, ctas in [(1 * MIB, L.ALGO_TWOSHOT, 32), (0, L.ALGO_ONESHOT, 8), (1 << 40, L.ALGO_TWOSHOT, 3),
-                            (4 * MIB, L.ALGO_ONESHOT, 64)]:
-        ins, outs, offs = run_emulated(ns, "fp32", cap, W, algo, options={L.OPT_COMM_CTAS: ctas})
+    for cap, algo, ctas, stage in [(1 * MIB, L.ALGO_TWOSHOT, 32, 0), (0, L.ALGO_ONESHOT, 8, 0),
+                                   (1 << 40, L.ALGO_TWOSHOT, 3, 0), (4 * MIB, L.ALGO_ONESHOT, 64, 0),
+                                   (1 << 40, L.ALGO_TWOSHOT, 5, 16 << 10), (2 * MIB, L.ALGO_ONESHOT, 7, 8 << 10)]:
+        ins, outs, offs = run_emulated(ns, "fp32", cap, W, algo,
+                                       options={L.OPT_COMM_CTAS: ctas, L.OPT_P2P_STAGE_BYTES: stage})
         if base is None:
             base = outs[0]
             _check_bitfaithful(ins, outs, offs, ns, "fp32", W)
