@@ -103,6 +103,9 @@ struct ddp_ctx {
   uint32_t* err_dev = nullptr;
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> event_pool;
+  // scratch for world-1 group launches
+  std::vector<int64_t> g_off, g_dst;
+  std::vector<void*> g_grad;
 };
 
 namespace {
@@ -206,7 +209,7 @@ void plan(ddp_ctx* c) {
     bk.byte_off = pos;
     pos += align_up(bk.numel * c->esize, 256);
     if (bk.algo == DDP_ALGO_TWOSHOT) l2max = std::max(l2max, align_up(cdiv(bk.numel, c->world), kAlignElems));
-    if (bk.algo == DDP_ALGO_ONESHOT) n1max = std::max(n1max, align_up(bk.numel, kAlignElems));
+    if (bk.algo == DDP_ALGO_ONESHOT && c->world > 1) n1max = std::max(n1max, align_up(bk.numel, kAlignElems));
   }
   c->stage2_stride = align_up(l2max * c->esize, 256);
   c->stage2_off = pos;
@@ -277,6 +280,9 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   if (bk.algo == DDP_ALGO_TWOSHOT) {
     a.stage_byte_off = c->stage2_off;
     a.stage_stride = c->stage2_stride;
+  } else if (c->world == 1) {
+    a.stage_byte_off = bk.byte_off;  // world 1 packs straight into the bucket
+    a.stage_stride = 0;
   } else {
     a.stage_byte_off = c->stage1_off + (int64_t)(c->p2p_launches & 1) * c->world * c->stage1_stride;
     a.stage_stride = c->stage1_stride;
@@ -302,10 +308,35 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   return DDP_OK;
 }
 
-// ---- a2/a5: launch bucket b (in order) ---------------------------------------
-ddp_status_t launch_bucket(ddp_ctx* c, int b, int32_t trigger) {
-  c->trace.emplace_back(b, trigger);
-  if (c->dry_run) return DDP_OK;
+// World 1: buckets [b0, b1) launched by one call run as ONE fused kernel over
+// the concatenation of their slots (pack into each bucket, 1-rank reduce and
+// unpack from registers); the values equal per-bucket launches bit for bit.
+ddp_status_t launch_local_group(ddp_ctx* c, int b0, int b1) {
+  c->g_off.clear();
+  c->g_grad.clear();
+  c->g_dst.clear();
+  int64_t base = 0;
+  for (int b = b0; b < b1; ++b) {
+    const Bucket& bk = c->buckets[b];
+    for (size_t s = 0; s < bk.params.size(); ++s) {
+      c->g_off.push_back(base + bk.off[s]);
+      c->g_grad.push_back(bk.grads[s]);
+      c->g_dst.push_back(bk.byte_off + bk.off[s] * c->esize);
+    }
+    base += bk.numel;
+  }
+  c->g_off.push_back(base);
+  const GroupView gv{c->g_off.data(), c->g_grad.data(), c->g_dst.data(), (int32_t)c->g_grad.size()};
+  prof_begin(c, 3);
+  CUDA_TRY(c, launch_local(c->dtype, gv, c->storage[c->rank], (int)c->pack_ctas, c->comm));
+  prof_end(c);
+  return DDP_OK;
+}
+
+// ---- a2/a5: launch buckets [b0, b1) (in order), triggered by ready signal t --
+ddp_status_t launch_range(ddp_ctx* c, int b0, int b1, int32_t trigger) {
+  for (int b = b0; b < b1; ++b) c->trace.emplace_back(b, trigger);
+  if (c->dry_run || b0 >= b1) return DDP_OK;
   // comm stream waits for everything the producers enqueued so far
   for (cudaStream_t s : c->unwaited) {
     cudaEvent_t ev = nullptr;
@@ -319,7 +350,28 @@ ddp_status_t launch_bucket(ddp_ctx* c, int b, int32_t trigger) {
     CUDA_TRY(c, cudaStreamWaitEvent(c->comm, ev, 0));
   }
   c->unwaited.clear();
-  return launch_device(c, b);
+  if (c->world == 1 && !c->emulated) {
+    // group maximal runs of world-1 fused buckets (slot table <= kMaxSlotsPerLaunch)
+    int b = b0;
+    while (b < b1) {
+      if (c->buckets[b].algo != DDP_ALGO_ONESHOT) {
+        if (ddp_status_t st = launch_device(c, b)) return st;
+        ++b;
+        continue;
+      }
+      int e = b;
+      size_t slots = 0;
+      while (e < b1 && c->buckets[e].algo == DDP_ALGO_ONESHOT &&
+             slots + c->buckets[e].params.size() <= (size_t)kMaxSlotsPerLaunch)
+        slots += c->buckets[e++].params.size();
+      if (ddp_status_t st = launch_local_group(c, b, e)) return st;
+      b = e;
+    }
+    return DDP_OK;
+  }
+  for (int b = b0; b < b1; ++b)
+    if (ddp_status_t st = launch_device(c, b)) return st;
+  return DDP_OK;
 }
 
 void open_pass(ddp_ctx* c) {
@@ -346,12 +398,11 @@ ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s) {
   if (std::find(c->unwaited.begin(), c->unwaited.end(), s) == c->unwaited.end()) c->unwaited.push_back(s);
   if (!c->overlap) return DDP_OK;
   const int32_t nb = (int32_t)c->buckets.size();
-  while (c->cursor < nb && c->pending[c->cursor] == 0) {
-    ddp_status_t st = launch_bucket(c, c->cursor, t);
-    if (st != DDP_OK) return st;
-    c->cursor++;
-  }
-  return DDP_OK;
+  int32_t e = c->cursor;
+  while (e < nb && c->pending[e] == 0) ++e;  // every consecutive ready bucket (C-7)
+  const int32_t b0 = c->cursor;
+  c->cursor = e;
+  return launch_range(c, b0, e, t);
 }
 
 bool is_layout_key(int32_t k) {
@@ -559,11 +610,9 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
   }
   if (!c->pass_no_sync) {
     const int32_t nb = (int32_t)c->buckets.size();
-    while (c->cursor < nb) {  // OVERLAP=0: all launches at finalize, in order
-      ddp_status_t st = launch_bucket(c, c->cursor, c->n_ready);
-      if (st != DDP_OK) return st;
-      c->cursor++;
-    }
+    const int32_t b0 = c->cursor;  // OVERLAP=0: all launches at finalize, in order
+    c->cursor = nb;
+    if (ddp_status_t st = launch_range(c, b0, nb, c->n_ready)) return st;
     if (!c->dry_run) {
       CUDA_TRY(c, cudaEventRecord(c->comm_done, c->comm));
       CUDA_TRY(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), c->comm_done, 0));

@@ -44,7 +44,18 @@ struct P2PLaunch {
   uint32_t* err;              // device-visible error word (mapped pinned host memory)
 };
 
+// Several buckets launched together at world 1: slot k covers virtual elements
+// [off[k], off[k+1]) of the concatenated buckets and packs to storage byte
+// offset dst[k].
+struct GroupView {
+  const int64_t* off;   // n+1 virtual offsets
+  void* const* grad;    // n gradient pointers
+  const int64_t* dst;   // n bucket byte offsets (inside the storage)
+  int32_t n;
+};
+
 // dtype: 0 = fp32, 1 = bf16 (ddp_dtype_t).
+cudaError_t launch_local(int dtype, const GroupView& gv, void* storage, int max_ctas, cudaStream_t s);
 cudaError_t launch_pack(int dtype, const SlotView& sv, void* bucket, float scale, int max_ctas,
                         cudaStream_t s);
 cudaError_t launch_unpack(int dtype, const SlotView& sv, const void* bucket, int max_ctas,

@@ -94,7 +94,7 @@ __device__ __forceinline__ void cta_xfer(T* const (&dst)[ND], const T* const (&s
                                          float s) {
   using E = Elem<T>;
   constexpr int VE = E::VE;
-  constexpr int U = NS >= 4 ? 1 : 4 / NS;
+  constexpr int U = NS == 1 ? 8 : (NS >= 4 ? 1 : 4 / NS);
   const int tid = threadIdx.x, nt = blockDim.x;
   if (n <= 0) return;
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(dst[0]) & 15;

@@ -99,7 +99,7 @@ __device__ __forceinline__ T* at(void* base, int64_t byte_off) {
 // stage k-1 and unpacks stage k-2, so NVLink stores of one stage overlap the
 // local reduction / unpack of the previous ones.
 template <typename T, int W, int MAXS>
-__global__ void __launch_bounds__(kThreads, W <= 2 ? 2 : 1)
+__global__ void __launch_bounds__(kThreads, 1)
     twoshot_kernel(const __grid_constant__ SlotArgs<MAXS> sa, const __grid_constant__ P2PLaunch a) {
   const int r = a.emulated ? (int)blockIdx.y : a.rank;
   const int64_t gstride = a.emulated ? (int64_t)r * a.grad_rank_stride : 0;
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kThreads, W <= 2 ? 2 : 1)
 // slot r of every rank and reduces stage k-1 (W local slots, rank order)
 // straight into the gradients.  Staging is double-buffered by launch parity.
 template <typename T, int W, int MAXS>
-__global__ void __launch_bounds__(kThreads, W <= 2 ? 2 : 1)
+__global__ void __launch_bounds__(kThreads, 1)
     oneshot_kernel(const __grid_constant__ SlotArgs<MAXS> sa, const __grid_constant__ P2PLaunch a) {
   const int r = a.emulated ? (int)blockIdx.y : a.rank;
   const int64_t gstride = a.emulated ? (int64_t)r * a.grad_rank_stride : 0;

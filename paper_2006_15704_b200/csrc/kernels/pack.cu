@@ -20,7 +20,7 @@ namespace {
 constexpr int64_t kTileBytes = (int64_t)kThreads * 16 * 4;  // 4 vectors per thread
 
 template <typename T, int MAXS>
-__global__ void __launch_bounds__(kThreads) pack_kernel(const __grid_constant__ SlotArgs<MAXS> sa,
+__global__ void __launch_bounds__(kThreads, 2) pack_kernel(const __grid_constant__ SlotArgs<MAXS> sa,
                                                         T* __restrict__ bucket, float s) {
   constexpr int64_t tile = kTileBytes / sizeof(T);
   const int64_t lo0 = sa.off[0], hi0 = sa.off[sa.n];
