@@ -106,6 +106,9 @@ struct ddp_ctx {
   // scratch for world-1 group launches
   std::vector<int64_t> g_off, g_dst;
   std::vector<void*> g_grad;
+  // batched ready signals: device launches deferred to the end of the batch
+  bool defer = false;
+  int32_t defer_b0 = 0, defer_b1 = 0;
 };
 
 namespace {
@@ -333,10 +336,25 @@ ddp_status_t launch_local_group(ddp_ctx* c, int b0, int b1) {
   return DDP_OK;
 }
 
+ddp_status_t device_range(ddp_ctx* c, int b0, int b1);
+
 // ---- a2/a5: launch buckets [b0, b1) (in order), triggered by ready signal t --
+// Inside ddp_grads_ready (a batch of ready signals that arrive together) the
+// device launch is deferred to the end of the batch so consecutive buckets can
+// share launches; the launch order and trace are unchanged.
 ddp_status_t launch_range(ddp_ctx* c, int b0, int b1, int32_t trigger) {
   for (int b = b0; b < b1; ++b) c->trace.emplace_back(b, trigger);
   if (c->dry_run || b0 >= b1) return DDP_OK;
+  if (c->defer) {
+    if (c->defer_b0 == c->defer_b1) c->defer_b0 = b0;
+    c->defer_b1 = b1;
+    return DDP_OK;
+  }
+  return device_range(c, b0, b1);
+}
+
+ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
+  if (b0 >= b1) return DDP_OK;
   // comm stream waits for everything the producers enqueued so far
   for (cudaStream_t s : c->unwaited) {
     cudaEvent_t ev = nullptr;
@@ -590,12 +608,21 @@ ddp_status_t ddp_grads_ready(ddp_ctx_t* c, int32_t n, const int32_t* params, voi
   if (ddp_status_t st = check_ctx(c)) return st;
   if (!c->bound && !c->dry_run) return fail(DDP_ERR_STATE, "context not bound to a device");
   if (n < 0 || (n > 0 && (!params || (!grads && !c->dry_run)))) return fail(DDP_ERR_INVALID_ARG, "bad batch");
-  for (int32_t i = 0; i < n; ++i) {
-    ddp_status_t st = grad_ready_one(c, params[i], grads ? grads[i] : nullptr,
-                                     static_cast<cudaStream_t>(producer_stream));
-    if (st != DDP_OK) return st;
+  c->defer = true;
+  c->defer_b0 = c->defer_b1 = 0;
+  ddp_status_t st = DDP_OK;
+  for (int32_t i = 0; i < n && st == DDP_OK; ++i)
+    st = grad_ready_one(c, params[i], grads ? grads[i] : nullptr, static_cast<cudaStream_t>(producer_stream));
+  c->defer = false;
+  // buckets completed by the batch are launched even if a later signal failed:
+  // their launch is already part of the (cross-rank) launch sequence
+  const std::string err = g_err;
+  ddp_status_t st2 = device_range(c, c->defer_b0, c->defer_b1);
+  if (st != DDP_OK) {
+    g_err = err;
+    return st;
   }
-  return DDP_OK;
+  return st2;
 }
 
 ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
