@@ -53,6 +53,10 @@ def parse():
     ap.add_argument("--comm-ctas", type=int, default=0)
     ap.add_argument("--pack-ctas", type=int, default=0)
     ap.add_argument("--stage-kib", type=int, default=0)
+    ap.add_argument("--exposed-model", default="resnet50", choices=["none", "resnet50", "bert_large"],
+                    help="real-model backward for the exposed-time measurement")
+    ap.add_argument("--exposed-batch", type=int, default=0)
+    ap.add_argument("--exposed-iters", type=int, default=10)
     ap.add_argument("--oneshot-max", type=int, default=-1)
     ap.add_argument("--twoshot-max", type=int, default=-1)
     return ap.parse_args()
@@ -248,7 +252,8 @@ def run_ours(a):
     algos = red.bucket_algos()
     bnumel = red.bucket_numels()
     S_tot = sum(bnumel) * esize
-    launches_per_step = sum(1 if x != "nccl" else 2 for x in algos)
+    # our kernel launches per step (NCCL's own kernels excluded)
+    launches_per_step = sum(prof[k][1] for k in ("pack", "unpack", "p2p_fused")) / kprof_steps
 
     # dominant kernel roofline: algorithmic bytes per launch / measured launch time
     peak_hbm, peak_src = measured_peaks()
@@ -258,19 +263,21 @@ def run_ours(a):
     if dom is not None:
         tot_ms, cnt = kinds[dom]
         avg_ms = tot_ms / cnt
+        per_step_launches = cnt / kprof_steps
         p2p = [(n * esize, x) for n, x in zip(bnumel, algos) if x != "nccl"]
         ncl = [n * esize for n, x in zip(bnumel, algos) if x == "nccl"]
         if dom == "p2p_fused" and world == 1:
             # world 1 fused kernel: read grad S, write bucket S, write grad S (3 S per bucket)
-            byts, bound, per = 3 * sum(b for b, _ in p2p) / len(p2p), "hbm", "3 x bucket bytes"
+            step_bytes, bound, per = 3 * sum(b for b, _ in p2p), "hbm", "3 x bucket bytes"
         elif dom in ("pack", "unpack"):
-            byts, bound, per = 2 * sum(ncl) / len(ncl), "hbm", "2 x bucket bytes"
+            step_bytes, bound, per = 2 * sum(ncl), "hbm", "2 x bucket bytes"
         elif dom == "p2p_fused":
             # NVLink bytes sent per GPU per direction: one-shot (W-1) S, two-shot 2 (W-1)/W S
-            byts = sum(b * ((world - 1) if x == "oneshot" else 2 * (world - 1) / world) for b, x in p2p) / len(p2p)
+            step_bytes = sum(b * ((world - 1) if x == "oneshot" else 2 * (world - 1) / world) for b, x in p2p)
             bound, per = "nvlink", "NVLink bytes per direction: one-shot (W-1)S, two-shot 2(W-1)/W S"
         else:
-            byts, bound, per = 2 * (world - 1) / world * sum(ncl) / len(ncl), "nvlink", "2(W-1)/W x bucket bytes"
+            step_bytes, bound, per = 2 * (world - 1) / world * sum(ncl), "nvlink", "2(W-1)/W x bucket bytes"
+        byts = step_bytes / per_step_launches
         peak = peak_hbm if bound == "hbm" else 770.0
         roof = {"bound": bound, "achieved": byts / (avg_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s"}
         roof["frac"] = roof["achieved"] / roof["peak"]
@@ -335,6 +342,10 @@ def run_ours(a):
     host_us = (t1 - t0) / len(order) * 1e6
 
     red.check_errors()
+    red.close()
+    exposed = None
+    if a.exposed_model != "none":
+        exposed = measure_exposed(a, rank, world, local, dev, opts)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         from oracle.cpu_baseline import time_sync
@@ -355,18 +366,113 @@ def run_ours(a):
                        "ready_order": "reverse registration, one batched ddp_grads_ready per step",
                        "parallelism": f"dp{world}"},
             "busbw": busbw,
+            "exposed": exposed,
             "roofline": roof,
             "kernel_ms_per_step": {k: v[0] / kprof_steps for k, v in prof.items() if v[1]},
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": launches_per_step * a.steps,
+            "gpu_launches": int(round(launches_per_step * a.steps)),
             "host_us_per_grad_ready": host_us,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
-    red.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_exposed(a, rank, world, local, dev, opts):
+    """Exposed (non-overlapped) sync time with a REAL backward:
+    the DDP front end's post-accumulate hooks drive the library during
+    loss.backward() of a randomly initialised model on synthetic data.
+    T_sync: event before backward() -> event after it returns (the finalize
+    callback has made the stream wait for the comm stream).  T_bwd: the same
+    window inside no_sync (hooks still fire and return early).  Interleaved
+    pairs; exposed = median(T_sync) - median(T_bwd), max over ranks."""
+    import statistics
+
+    import torch
+    import torch.distributed as dist
+    from paper_2006_15704_b200.ddp import DistributedDataParallel
+
+    torch.backends.cudnn.benchmark = True
+    torch.backends.cuda.matmul.allow_tf32 = True
+    torch.backends.cudnn.allow_tf32 = True
+    g = torch.Generator(device=dev).manual_seed(15704 + rank)
+    if a.exposed_model == "resnet50":
+        import torchvision
+        model = torchvision.models.resnet50().to(dev)
+        B = a.exposed_batch or 64
+        x = torch.randn(B, 3, 224, 224, device=dev, generator=g)
+        y = torch.randint(0, 1000, (B,), device=dev, generator=g)
+        lossf = torch.nn.CrossEntropyLoss()
+
+        def fwd(m):
+            return lossf(m(x), y)
+        desc = f"torchvision resnet50, batch {B}/GPU, 224x224, CrossEntropy"
+    else:
+        import transformers
+        cfg = transformers.BertConfig(hidden_size=1024, num_hidden_layers=24, num_attention_heads=16,
+                                      intermediate_size=4096)
+        model = transformers.BertModel(cfg).to(dev)
+        B, S = (a.exposed_batch or 8), 512
+        ids = torch.randint(0, cfg.vocab_size, (B, S), device=dev, generator=g)
+
+        def fwd(m):
+            return m(input_ids=ids).last_hidden_state.float().pow(2).mean()
+        desc = f"HF BertModel-large, {B}x{S} tokens/GPU, mean-square loss"
+    if a.dtype == "bf16":
+        model = model.to(torch.bfloat16)
+        if a.exposed_model == "resnet50":
+            x = x.to(torch.bfloat16)
+    ddp = DistributedDataParallel(model, bucket_cap_mb=a.cap_mib, options=opts)
+    stream = torch.cuda.current_stream(dev)
+
+    def one(sync: bool) -> float:
+        for p in ddp.params:
+            p.grad = None
+        loss = fwd(ddp)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if sync:
+            s.record(stream)
+            loss.backward()
+            e.record(stream)
+        else:
+            with ddp.no_sync():
+                s.record(stream)
+                loss.backward()
+                e.record(stream)
+        torch.cuda.synchronize(dev)
+        return s.elapsed_time(e)
+
+    for _ in range(3):
+        one(True)
+        one(False)
+    if world > 1:
+        dist.barrier(device_ids=[local])
+    from paper_2006_15704_b200 import _lib as L
+    ts, tb, tn = [], [], []
+    for _ in range(a.exposed_iters):
+        ts.append(one(True))
+        tb.append(one(False))
+        ddp.reducer.set_option(L.OPT_OVERLAP, 0)   # paper's non-overlapped baseline (P:L399)
+        tn.append(one(True))
+        ddp.reducer.set_option(L.OPT_OVERLAP, 1)
+    ddp.reducer.check_errors()
+    vals = torch.tensor([statistics.median(ts), statistics.median(tb), statistics.median(tn)],
+                        dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    t_sync, t_bwd, t_noov = float(vals[0]), float(vals[1]), float(vals[2])
+    res = {"model": desc, "dtype": a.dtype, "bucket_cap_mib": a.cap_mib,
+           "buckets": ddp.reducer.num_buckets, "bucket_algos": ddp.reducer.bucket_algos(),
+           "t_bwd_ms": t_bwd, "t_bwd_plus_sync_ms": t_sync, "exposed_ms": t_sync - t_bwd,
+           "exposed_pct_of_bwd": 100.0 * (t_sync - t_bwd) / t_bwd,
+           "t_bwd_plus_sync_no_overlap_ms": t_noov, "exposed_no_overlap_ms": t_noov - t_bwd,
+           "iters": a.exposed_iters, "timing": "median of interleaved triples, max over ranks"}
+    ddp.reducer.close()
+    del ddp, model
+    torch.cuda.empty_cache()
+    return res
 
 
 def main():

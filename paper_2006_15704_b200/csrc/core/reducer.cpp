@@ -76,7 +76,7 @@ struct ddp_ctx {
   std::vector<int64_t> p_off;
   // options
   int64_t overlap = 1, oneshot_max = 256 * 1024, twoshot_max = INT64_MAX, comm_ctas = 32,
-          dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 2, stage_bytes = 0;
+          dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 8, stage_bytes = 0;
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
           stage1_stride = 0, storage_bytes = 0;
