@@ -417,9 +417,10 @@ def measure_exposed(a, rank, world, local, dev, opts):
         B, S = (a.exposed_batch or 8), 512
         ids = torch.randint(0, cfg.vocab_size, (B, S), device=dev, generator=g)
 
-        def fwd(m):
-            return m(input_ids=ids).last_hidden_state.float().pow(2).mean()
-        desc = f"HF BertModel-large, {B}x{S} tokens/GPU, mean-square loss"
+        def fwd(m):  # touches every parameter (pooler included): no unused parameters
+            o = m(input_ids=ids)
+            return o.last_hidden_state.float().pow(2).mean() + o.pooler_output.float().pow(2).mean()
+        desc = f"HF BertModel-large, {B}x{S} tokens/GPU, mean-square loss on hidden states + pooler"
     if a.dtype == "bf16":
         model = model.to(torch.bfloat16)
         if a.exposed_model == "resnet50":

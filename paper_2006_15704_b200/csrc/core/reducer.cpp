@@ -75,7 +75,9 @@ struct ddp_ctx {
   std::vector<int32_t> p_bucket, p_slot;
   std::vector<int64_t> p_off;
   // options
-  int64_t overlap = 1, oneshot_max = 256 * 1024, twoshot_max = INT64_MAX, comm_ctas = 32,
+  // oneshot_max < 0: automatic (world 2: every bucket one-shot — it sends the same
+  // NVLink bytes as two-shot with one sync instead of two; world > 2: <= 512 KiB)
+  int64_t overlap = 1, oneshot_max = -1, twoshot_max = INT64_MAX, comm_ctas = 64,
           dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 8, stage_bytes = 0;
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
@@ -167,7 +169,8 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   int a;
   if (c->algo != DDP_ALGO_AUTO) a = (int)c->algo;
   else if (c->world == 1) a = DDP_ALGO_ONESHOT;
-  else if (bytes <= c->oneshot_max) a = DDP_ALGO_ONESHOT;
+  else if (bytes <= (c->oneshot_max >= 0 ? c->oneshot_max : c->world == 2 ? INT64_MAX : 512 * 1024))
+    a = DDP_ALGO_ONESHOT;
   else if (bytes <= c->twoshot_max) a = DDP_ALGO_TWOSHOT;
   else a = DDP_ALGO_NCCL;
   if (a != DDP_ALGO_NCCL && (int)bk.params.size() > kMaxSlotsPerLaunch) a = DDP_ALGO_NCCL;
