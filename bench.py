@@ -57,6 +57,7 @@ def parse():
                     help="real-model backward for the exposed-time measurement")
     ap.add_argument("--exposed-batch", type=int, default=0)
     ap.add_argument("--exposed-iters", type=int, default=10)
+    ap.add_argument("--timeline-detail", action="store_true", help="include per-launch timeline in the JSON")
     ap.add_argument("--oneshot-max", type=int, default=-1)
     ap.add_argument("--twoshot-max", type=int, default=-1)
     return ap.parse_args()
@@ -458,6 +459,21 @@ def measure_exposed(a, rank, world, local, dev, opts):
         ddp.reducer.set_option(L.OPT_OVERLAP, 0)   # paper's non-overlapped baseline
         tn.append(one(True))
         ddp.reducer.set_option(L.OPT_OVERLAP, 1)
+    # one profiled synced pass: Fig. 2(c)-style ready / start / end timeline of the comm launches
+    ddp.reducer.set_option(L.OPT_PROFILE, 1)
+    L.ddp_profile_timeline(ddp.reducer.ctx)
+    one(True)
+    tl = L.ddp_profile_timeline(ddp.reducer.ctx)
+    ddp.reducer.set_option(L.OPT_PROFILE, 0)
+    timeline = None
+    if tl:
+        timeline = {"launches": len(tl), "last_ready_ms": max(r for _, r, _, _ in tl),
+                    "last_end_ms": max(e for _, _, _, e in tl),
+                    "tail_ms": max(e for _, _, _, e in tl) - max(r for _, r, _, _ in tl),
+                    "max_queue_delay_ms": max(s - r for _, r, s, _ in tl),
+                    "comm_busy_ms": sum(e - s for _, _, s, e in tl),
+                    "per_launch": [[k, round(r, 4), round(s, 4), round(e, 4)] for k, r, s, e in tl]
+                    if a.timeline_detail else None}
     ddp.reducer.check_errors()
     vals = torch.tensor([statistics.median(ts), statistics.median(tb), statistics.median(tn)],
                         dtype=torch.float64, device=dev)
@@ -469,7 +485,8 @@ def measure_exposed(a, rank, world, local, dev, opts):
            "t_bwd_ms": t_bwd, "t_bwd_plus_sync_ms": t_sync, "exposed_ms": t_sync - t_bwd,
            "exposed_pct_of_bwd": 100.0 * (t_sync - t_bwd) / t_bwd,
            "t_bwd_plus_sync_no_overlap_ms": t_noov, "exposed_no_overlap_ms": t_noov - t_bwd,
-           "iters": a.exposed_iters, "timing": "median of interleaved triples, max over ranks"}
+           "iters": a.exposed_iters, "timing": "median of interleaved triples, max over ranks",
+           "timeline_rank0": timeline if rank == 0 else None}
     ddp.reducer.close()
     del ddp, model
     torch.cuda.empty_cache()

@@ -167,6 +167,13 @@ ddp_status_t ddp_launch_trace(const ddp_ctx_t* ctx, int32_t* buckets, int32_t* t
  * summed device milliseconds and launch counts since the last read, per kind
  * [0]=pack [1]=NCCL allreduce [2]=unpack [3]=fused P2P kernel; then clears. */
 ddp_status_t ddp_profile_read(ddp_ctx_t* ctx, double ms[4], int64_t launches[4]);
+/* With DDP_OPT_PROFILE=1: per device launch since the last read (in launch
+ * order), its kind (as above), the time its bucket(s) became ready on the
+ * producer stream, and its start / end on the comm stream, in ms relative to
+ * the first recorded ready point (the Fig. 2(c)-style ready/launch/done
+ * timeline).  *n receives the count; at most cap entries are written; clears. */
+ddp_status_t ddp_profile_timeline(ddp_ctx_t* ctx, int32_t cap, int32_t* kinds, double* ready_ms,
+                                  double* start_ms, double* end_ms, int32_t* n);
 /* Checks the device-side error word (P2P barrier timeout). */
 ddp_status_t ddp_check_device_errors(ddp_ctx_t* ctx);
 const char* ddp_last_error(void);

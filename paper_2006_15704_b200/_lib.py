@@ -61,6 +61,8 @@ _SIGS = {
     "ddp_launch_trace": (C.c_int, [_P, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32,
                                    C.POINTER(C.c_int32)]),
     "ddp_profile_read": (C.c_int, [_P, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    "ddp_profile_timeline": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int32)]),
     "ddp_check_device_errors": (C.c_int, [_P]),
     "ddp_last_error": (C.c_char_p, []),
     "ddp_version": (C.c_char_p, []),
@@ -205,6 +207,15 @@ def ddp_profile_read(ctx: int):
     cnt = (C.c_int64 * 4)()
     _check(lib().ddp_profile_read(ctx, ms, cnt))
     return {k: (ms[i], cnt[i]) for i, k in enumerate(PROFILE_KINDS)}
+
+
+def ddp_profile_timeline(ctx: int, cap: int = 4096):
+    """[(kind, ready_ms, start_ms, end_ms)] per device launch since the last read."""
+    k = (C.c_int32 * cap)()
+    r, s, e = (C.c_double * cap)(), (C.c_double * cap)(), (C.c_double * cap)()
+    n = C.c_int32()
+    _check(lib().ddp_profile_timeline(ctx, cap, k, r, s, e, C.byref(n)))
+    return [(PROFILE_KINDS[k[i]], r[i], s[i], e[i]) for i in range(min(cap, n.value))]
 
 
 def ddp_check_device_errors(ctx: int) -> None:

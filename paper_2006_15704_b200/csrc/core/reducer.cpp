@@ -62,6 +62,7 @@ enum class State { CREATED, IDLE, IN_PASS };
 struct ProfRec {
   int kind;
   cudaEvent_t a, b;
+  int ready;  // index into ddp_ctx::prof_ready (producer-stream event at launch time)
 };
 
 }  // namespace
@@ -104,6 +105,7 @@ struct ddp_ctx {
   uint32_t* err_host = nullptr;
   uint32_t* err_dev = nullptr;
   std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> prof_ready;
   std::vector<cudaEvent_t> event_pool;
   // scratch for world-1 group launches
   std::vector<int64_t> g_off, g_dst;
@@ -250,7 +252,7 @@ cudaEvent_t pool_event(ddp_ctx* c) {
 }
 void prof_begin(ddp_ctx* c, int kind) {
   if (!c->profile) return;
-  ProfRec r{kind, pool_event(c), pool_event(c)};
+  ProfRec r{kind, pool_event(c), pool_event(c), (int)c->prof_ready.size() - 1};
   cudaEventRecord(r.a, c->comm);
   c->prof.push_back(r);
 }
@@ -358,6 +360,11 @@ ddp_status_t launch_range(ddp_ctx* c, int b0, int b1, int32_t trigger) {
 
 ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
   if (b0 >= b1) return DDP_OK;
+  if (c->profile) {  // when the producer reached this launch point (timeline "ready")
+    cudaEvent_t ev = pool_event(c);
+    CUDA_TRY(c, cudaEventRecord(ev, c->unwaited.empty() ? c->comm : c->unwaited.front()));
+    c->prof_ready.push_back(ev);
+  }
   // comm stream waits for everything the producers enqueued so far
   for (cudaStream_t s : c->unwaited) {
     cudaEvent_t ev = nullptr;
@@ -485,6 +492,7 @@ void ddp_destroy(ddp_ctx_t* c) {
     cudaEventDestroy(r.b);
   }
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->prof_ready) cudaEventDestroy(e);
   if (c->comm_done) cudaEventDestroy(c->comm_done);
   if (c->err_host) cudaFreeHost(c->err_host);
   delete c;
@@ -757,10 +765,37 @@ ddp_status_t ddp_profile_read(ddp_ctx_t* c, double ms[4], int64_t launches[4]) {
     CUDA_TRY(c, cudaEventElapsedTime(&t, r.a, r.b));
     ms[r.kind] += t;
     launches[r.kind] += 1;
+  }
+  return ddp_profile_timeline(c, 0, nullptr, nullptr, nullptr, nullptr, nullptr);
+}
+
+ddp_status_t ddp_profile_timeline(ddp_ctx_t* c, int32_t cap, int32_t* kinds, double* ready_ms, double* start_ms,
+                                  double* end_ms, int32_t* n) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (cap < 0) return fail(DDP_ERR_INVALID_ARG, "negative cap");
+  if (n) *n = (int32_t)c->prof.size();
+  cudaEvent_t base = c->prof_ready.empty() ? nullptr : c->prof_ready.front();
+  for (size_t i = 0; i < c->prof.size(); ++i) {
+    const ProfRec& r = c->prof[i];
+    CUDA_TRY(c, cudaEventSynchronize(r.b));
+    if ((int32_t)i < cap && base) {
+      float t0 = 0, t1 = 0, t2 = 0;
+      if (r.ready >= 0) CUDA_TRY(c, cudaEventElapsedTime(&t0, base, c->prof_ready[r.ready]));
+      CUDA_TRY(c, cudaEventElapsedTime(&t1, base, r.a));
+      CUDA_TRY(c, cudaEventElapsedTime(&t2, base, r.b));
+      if (kinds) kinds[i] = r.kind;
+      if (ready_ms) ready_ms[i] = t0;
+      if (start_ms) start_ms[i] = t1;
+      if (end_ms) end_ms[i] = t2;
+    }
+  }
+  for (auto& r : c->prof) {
     c->event_pool.push_back(r.a);
     c->event_pool.push_back(r.b);
   }
+  for (cudaEvent_t e : c->prof_ready) c->event_pool.push_back(e);
   c->prof.clear();
+  c->prof_ready.clear();
   return DDP_OK;
 }
 

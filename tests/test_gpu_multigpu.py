@@ -2,12 +2,15 @@
 torch symmetric memory for the peer-mapped storage).  Skipped with < 2 GPUs.
 
 Each rank fills rank-specific synthetic gradients on its own GPU, runs synced
-passes through ``ddp.GradReducer`` (the C ABI), and returns its outputs; the
-parent compares them with the oracle: P2P paths bit-exact vs O-3b and
-identical across ranks; NCCL path within the fp32/bf16 tolerances."""
+passes through ``ddp.GradReducer`` (the C ABI) and returns, per parameter, an
+exact checksum of its whole output plus the output at sampled indices (all
+elements for small tensors).  The parent checks replica consistency (equal
+checksums on every rank) and compares the sampled values with the oracle
+computed one by one from the host generator: P2P paths bit-exact vs O-3b;
+NCCL path fp32 |y-ref| <= 1e-6 den, bf16 normwise <= 1e-2."""
 
 import os
-import socket
+import tempfile
 
 import numpy as np
 import pytest
@@ -16,7 +19,7 @@ import torch.multiprocessing as mp
 
 from oracle.assignment import MIB
 from oracle.average import average_bitfaithful, average_fp64, to_fp32
-from synth.gen import gen_grads
+from synth.gen import gen_values
 from synth.shapes import numels
 
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
@@ -26,19 +29,18 @@ if NGPU < 2:
     pytest.skip("needs >= 2 GPUs", allow_module_level=True)
 
 
-def _port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+def _sample_idx(p: int, n: int, k: int = 2048) -> np.ndarray:
+    if n <= k:
+        return np.arange(n, dtype=np.int64)
+    rng = np.random.default_rng(1000 + p)
+    return np.unique(np.concatenate([rng.integers(0, n, k), [0, n - 1]])).astype(np.int64)
 
 
-def _worker(rank, world, port, cfgs, q):
-    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+def _worker(rank, world, init_file, cfgs, q):
     torch.cuda.set_device(rank)
     import torch.distributed as dist
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", rank))
+    dist.init_process_group("nccl", init_method=f"file://{init_file}", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
     from paper_2006_15704_b200 import _lib as L
     from paper_2006_15704_b200.ddp import GradReducer
     from synth import device as sdev
@@ -49,6 +51,7 @@ def _worker(rank, world, port, cfgs, q):
             ns = numels(model)
             red = GradReducer(ns, dtype, cap, options={L.OPT_ALGO: algo})
             grads = [torch.empty(n, dtype=TDT[dtype], device="cuda") for n in ns]
+            idx = [torch.from_numpy(_sample_idx(p, n)).cuda() for p, n in enumerate(ns)]
             res = []
             for it in range(iters):
                 sdev.fill_all(grads, 15704, rank, it, "normal", dtype)
@@ -56,7 +59,9 @@ def _worker(rank, world, port, cfgs, q):
                     red.grad_ready(p, grads[p])
                 red.finalize()
                 torch.cuda.synchronize()
-                res.append([to_np(g, dtype) for g in grads])
+                sums = [int(g.view(torch.int16 if dtype == "bf16" else torch.int32).to(torch.int64)
+                            .mul_(torch.arange(1, g.numel() + 1, device="cuda")).sum()) for g in grads]
+                res.append((sums, [to_np(g[i], dtype) for g, i in zip(grads, idx)]))
             red.check_errors()
             red.close()
             out.append(res)
@@ -70,13 +75,19 @@ def _worker(rank, world, port, cfgs, q):
 def _run(world, cfgs):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = _port()
-    ps = [ctx.Process(target=_worker, args=(r, world, port, cfgs, q)) for r in range(world)]
+    fd, init_file = tempfile.mkstemp(prefix="b200ddp_init_")
+    os.close(fd)
+    os.unlink(init_file)
+    ps = [ctx.Process(target=_worker, args=(r, world, init_file, cfgs, q)) for r in range(world)]
     for p in ps:
         p.start()
-    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda x: x[0])
-    for p in ps:
-        p.join(timeout=120)
+    try:
+        res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda x: x[0])
+    finally:
+        for p in ps:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
     for r, _, err in res:
         assert err is None, f"rank {r}: {err}"
     return [x[1] for x in res]
@@ -87,24 +98,24 @@ def test_multigpu_parity(world):
     from paper_2006_15704_b200 import _lib as L
     cfgs = [("toy", "fp32", 4096, L.ALGO_ONESHOT, 2), ("toy", "bf16", 4096, L.ALGO_TWOSHOT, 2),
             ("toy", "fp32", 4096, L.ALGO_NCCL, 1), ("resnet50", "fp32", 25 * MIB, L.ALGO_AUTO, 2),
-            ("resnet50", "bf16", 25 * MIB, L.ALGO_NCCL, 1)]
+            ("resnet50", "bf16", 25 * MIB, L.ALGO_TWOSHOT, 1), ("resnet50", "bf16", 25 * MIB, L.ALGO_NCCL, 1)]
     outs = _run(world, cfgs)
     for ci, (model, dtype, cap, algo, iters) in enumerate(cfgs):
         ns = numels(model)
         for it in range(iters):
-            ins = [gen_grads(ns, 15704, r, it, "normal", dtype) for r in range(world)]
             for p in range(len(ns)):
-                got = [outs[r][ci][it][p] for r in range(world)]
-                for r in range(1, world):                 # replica consistency
-                    assert np.array_equal(got[r], got[0]), (model, p)
-                xs = [ins[r][p] for r in range(world)]
+                sums = [outs[r][ci][it][0][p] for r in range(world)]
+                assert len(set(sums)) == 1, ("replicas differ (S:L303)", model, dtype, algo, p)
+                idx = _sample_idx(p, ns[p])
+                got = outs[0][ci][it][1][p]
+                xs = [gen_values(15704, r, it, p, idx, "normal", dtype) for r in range(world)]
                 if algo == L.ALGO_NCCL:
                     ref, den = average_fp64(xs, dtype)
-                    y = to_fp32(got[0], dtype).astype(np.float64)
+                    y = to_fp32(got, dtype).astype(np.float64)
                     r64 = to_fp32(ref, dtype).astype(np.float64)
                     if dtype == "fp32":
                         assert np.all(np.abs(y - r64) <= 1e-6 * den + 1e-45), (model, p)
                     else:
                         assert np.linalg.norm(y - r64) <= 1e-2 * np.linalg.norm(r64) + 1e-30, (model, p)
                 else:
-                    assert np.array_equal(got[0], average_bitfaithful(xs, dtype)), (model, dtype, algo, p)
+                    assert np.array_equal(got, average_bitfaithful(xs, dtype)), (model, dtype, algo, p)
