@@ -73,14 +73,21 @@ enum {
   DDP_OPT_COMM_CTAS = 4,        /* max CTAs of a P2P kernel when world > 1 (1..148) */
   DDP_OPT_DRY_RUN = 5,          /* 1: protocol only, no device work (host tests; CREATED only) */
   DDP_OPT_PROFILE = 6,          /* 1: time every device launch with CUDA events */
-  DDP_OPT_ALGO = 7,             /* force the bucket allreduce: 0 auto, 1 NCCL, 2 one-shot, 3 two-shot */
+  DDP_OPT_ALGO = 7,             /* force the bucket allreduce: 0 auto, 1 NCCL, 2 one-shot, 3 two-shot,
+                                   4 copy-engine one-shot (world > 1) */
   DDP_OPT_PACK_CTAS = 8,        /* max CTAs of pack/unpack kernels and of P2P kernels at world 1 */
   DDP_OPT_P2P_STAGE_BYTES = 9   /* 0 (default): one pipeline stage per CTA chunk; else split each
                                    CTA chunk into stages of this many bytes (one sync per stage) */
 };
 
-/* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO. */
-enum { DDP_ALGO_AUTO = 0, DDP_ALGO_NCCL = 1, DDP_ALGO_ONESHOT = 2, DDP_ALGO_TWOSHOT = 3 };
+/* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.
+ *   NCCL:    pack kernel -> ncclAllReduce(sum) -> unpack kernel
+ *   ONESHOT: one fused sm_100a kernel: pack, push to every peer, rank-order reduce into .grad
+ *   TWOSHOT: one fused sm_100a kernel: pack + reduce-scatter push, reduce, all-gather push, unpack
+ *   CE:      pack kernel -> copy-engine pushes (cudaMemcpyAsync over NVLink) ordered by stream
+ *            memory operations (no SM waits) -> rank-order reduce kernel into .grad on a second
+ *            stream.  Frees the SMs for the overlapped backward. */
+enum { DDP_ALGO_AUTO = 0, DDP_ALGO_NCCL = 1, DDP_ALGO_ONESHOT = 2, DDP_ALGO_TWOSHOT = 3, DDP_ALGO_CE = 4 };
 
 /* ---- construction (host only, deterministic, touches no GPU) -------------
  * Bucket assignment (Alg. 1 "allocate parameters to buckets in the
@@ -165,8 +172,9 @@ ddp_status_t ddp_launch_trace(const ddp_ctx_t* ctx, int32_t* buckets, int32_t* t
                               int32_t cap, int32_t* n);
 /* With DDP_OPT_PROFILE=1: synchronizes the recorded events and returns the
  * summed device milliseconds and launch counts since the last read, per kind
- * [0]=pack [1]=NCCL allreduce [2]=unpack [3]=fused P2P kernel; then clears. */
-ddp_status_t ddp_profile_read(ddp_ctx_t* ctx, double ms[4], int64_t launches[4]);
+ * [0]=pack [1]=NCCL allreduce [2]=unpack [3]=fused P2P kernel (incl. world-1 group)
+ * [4]=copy-engine pushes [5]=copy-engine reduce kernel; then clears. */
+ddp_status_t ddp_profile_read(ddp_ctx_t* ctx, double ms[6], int64_t launches[6]);
 /* With DDP_OPT_PROFILE=1: per device launch since the last read (in launch
  * order), its kind (as above), the time its bucket(s) became ready on the
  * producer stream, and its start / end on the comm stream, in ms relative to

@@ -24,9 +24,9 @@ STATUS_NAMES = ["OK", "INVALID_ARG", "STATE", "DUPLICATE", "INCOMPLETE", "CUDA",
 FP32, BF16 = 0, 1
 OPT_OVERLAP, OPT_P2P_ONESHOT_MAX, OPT_P2P_TWOSHOT_MAX, OPT_COMM_CTAS, OPT_DRY_RUN, OPT_PROFILE, \
     OPT_ALGO, OPT_PACK_CTAS, OPT_P2P_STAGE_BYTES = range(1, 10)
-ALGO_AUTO, ALGO_NCCL, ALGO_ONESHOT, ALGO_TWOSHOT = range(4)
-ALGO_NAMES = {ALGO_NCCL: "nccl", ALGO_ONESHOT: "oneshot", ALGO_TWOSHOT: "twoshot"}
-PROFILE_KINDS = ("pack", "nccl_allreduce", "unpack", "p2p_fused")
+ALGO_AUTO, ALGO_NCCL, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_CE = range(5)
+ALGO_NAMES = {ALGO_NCCL: "nccl", ALGO_ONESHOT: "oneshot", ALGO_TWOSHOT: "twoshot", ALGO_CE: "ce"}
+PROFILE_KINDS = ("pack", "nccl_allreduce", "unpack", "p2p_fused", "ce_copy", "ce_reduce")
 
 
 class DDPError(RuntimeError):
@@ -203,8 +203,8 @@ def ddp_launch_trace(ctx: int) -> List[Tuple[int, int]]:
 
 
 def ddp_profile_read(ctx: int):
-    ms = (C.c_double * 4)()
-    cnt = (C.c_int64 * 4)()
+    ms = (C.c_double * 6)()
+    cnt = (C.c_int64 * 6)()
     _check(lib().ddp_profile_read(ctx, ms, cnt))
     return {k: (ms[i], cnt[i]) for i, k in enumerate(PROFILE_KINDS)}
 

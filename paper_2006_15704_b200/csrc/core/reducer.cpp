@@ -10,6 +10,7 @@
 //   NCCL:                 pack kernel -> ncclAllReduce(sum) -> unpack kernel
 // The choice is a deterministic function of bucket bytes and options, so it
 // is identical on every rank (same order and content on all ranks).
+#include <cuda.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -55,6 +56,9 @@ struct Bucket {
   int ctas = 1;
   int64_t shard = 0, chunk = 0, sub = 0;
   int32_t stages = 0;
+  // copy-engine algorithm: W slots at ce_off + q * ce_stride; passes launched so far
+  int64_t ce_off = 0, ce_stride = 0;
+  uint32_t ce_count = 0;
 };
 
 enum class State { CREATED, IDLE, IN_PASS };
@@ -82,7 +86,14 @@ struct ddp_ctx {
           dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 8, stage_bytes = 0;
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
-          stage1_stride = 0, storage_bytes = 0;
+          stage1_stride = 0, ce_flags_off = 0, storage_bytes = 0;
+  // copy-engine path: reduce stream, events, driver stream-memory-op entry points
+  cudaStream_t ce_red = nullptr;
+  std::vector<cudaEvent_t> ce_packed;  // per bucket: own slot packed (comm -> reduce stream)
+  cudaEvent_t ce_red_done = nullptr;
+  void* fn_write32 = nullptr;
+  void* fn_wait32 = nullptr;
+  bool ce_used = false;  // a CE bucket was launched in the open pass
   // protocol state
   State state = State::CREATED;
   bool bound = false, emulated = false, poisoned = false;
@@ -169,13 +180,14 @@ void assign(ddp_ctx* c) {
 int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   const int64_t bytes = bk.numel * c->esize;
   int a;
-  if (c->algo != DDP_ALGO_AUTO) a = (int)c->algo;
+  if (c->algo != DDP_ALGO_AUTO) a = (c->algo == DDP_ALGO_CE && c->world == 1) ? DDP_ALGO_ONESHOT : (int)c->algo;
   else if (c->world == 1) a = DDP_ALGO_ONESHOT;
   else if (bytes <= (c->oneshot_max >= 0 ? c->oneshot_max : c->world == 2 ? INT64_MAX : 512 * 1024))
     a = DDP_ALGO_ONESHOT;
   else if (bytes <= c->twoshot_max) a = DDP_ALGO_TWOSHOT;
   else a = DDP_ALGO_NCCL;
-  if (a != DDP_ALGO_NCCL && (int)bk.params.size() > kMaxSlotsPerLaunch) a = DDP_ALGO_NCCL;
+  if ((a == DDP_ALGO_ONESHOT || a == DDP_ALGO_TWOSHOT) && (int)bk.params.size() > kMaxSlotsPerLaunch)
+    a = DDP_ALGO_NCCL;
   return a;
 }
 
@@ -225,6 +237,16 @@ void plan(ddp_ctx* c) {
   c->stage1_stride = align_up(n1max * c->esize, 256);
   c->stage1_off = pos;
   pos += 2 * c->world * c->stage1_stride;  // double-buffered by launch parity
+  // copy-engine buckets: W slots each (dedicated per bucket) + ready/consumed flags
+  c->ce_flags_off = pos;
+  pos += align_up((int64_t)c->buckets.size() * kMaxWorld * 2 * 4, 256);
+  for (Bucket& bk : c->buckets) {
+    bk.ce_stride = 0;
+    if (bk.algo != DDP_ALGO_CE) continue;
+    bk.ce_stride = align_up(bk.numel * c->esize, 256);
+    bk.ce_off = pos;
+    pos += c->world * bk.ce_stride;
+  }
   c->storage_bytes = pos;
   for (Bucket& bk : c->buckets) grid_for(c, bk, max_ctas_for(c, bk));
 }
@@ -250,15 +272,80 @@ cudaEvent_t pool_event(ddp_ctx* c) {
   cudaEventCreate(&e);
   return e;
 }
-void prof_begin(ddp_ctx* c, int kind) {
+void prof_begin(ddp_ctx* c, int kind, cudaStream_t s = nullptr) {
   if (!c->profile) return;
   ProfRec r{kind, pool_event(c), pool_event(c), (int)c->prof_ready.size() - 1};
-  cudaEventRecord(r.a, c->comm);
+  cudaEventRecord(r.a, s ? s : c->comm);
   c->prof.push_back(r);
 }
-void prof_end(ddp_ctx* c) {
+void prof_end(ddp_ctx* c, cudaStream_t s = nullptr) {
   if (!c->profile || c->prof.empty()) return;
-  cudaEventRecord(c->prof.back().b, c->comm);
+  cudaEventRecord(c->prof.back().b, s ? s : c->comm);
+}
+
+typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+// ce flags of bucket b in a rank's storage: [0][b][src] ready, [1][b][src] consumed
+uint32_t* ce_flag(const ddp_ctx* c, int r, int kind, int b, int src) {
+  return reinterpret_cast<uint32_t*>(static_cast<char*>(c->storage[r]) + c->ce_flags_off) +
+         ((size_t)kind * c->buckets.size() + b) * kMaxWorld + src;
+}
+
+ddp_status_t ce_write(ddp_ctx* c, cudaStream_t s, uint32_t* addr, uint32_t v) {
+  // default flags: a memory fence precedes the write (stream-scoped __threadfence_system)
+  CUresult r = reinterpret_cast<StreamValueFn>(c->fn_write32)((CUstream)s, (CUdeviceptr)addr, v, 0);
+  if (r != CUDA_SUCCESS) return cuda_fail(c, cudaErrorUnknown, "cuStreamWriteValue32");
+  return DDP_OK;
+}
+ddp_status_t ce_wait(ddp_ctx* c, cudaStream_t s, uint32_t* addr, uint32_t v) {
+  CUresult r = reinterpret_cast<StreamValueFn>(c->fn_wait32)((CUstream)s, (CUdeviceptr)addr, v,
+                                                              CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return cuda_fail(c, cudaErrorUnknown, "cuStreamWaitValue32");
+  return DDP_OK;
+}
+
+// Copy-engine one-shot (SM-free exchange): pack own slot (kernel) -> copy-engine
+// push of the slot into every peer (cudaMemcpyAsync over NVLink) -> flag writes;
+// on the reduce stream: wait for every peer's flag -> rank-order reduction of
+// the W slots straight into .grad (kernel) -> "consumed" flags, which guard the
+// next pass's pushes into this bucket's slots.  No SM spins while waiting.
+ddp_status_t launch_ce(ddp_ctx* c, int b, const SlotView& sv, float scale) {
+  Bucket& bk = c->buckets[b];
+  const int W = c->world, r = c->rank;
+  char* mine = static_cast<char*>(c->storage[r]);
+  const uint32_t v = ++bk.ce_count;
+  const int64_t bytes = bk.numel * c->esize;
+  if (v > 1)
+    for (int i = 1; i < W; ++i)
+      if (ddp_status_t st = ce_wait(c, c->comm, ce_flag(c, r, 1, b, (r + i) % W), v - 1)) return st;
+  prof_begin(c, 0);
+  CUDA_TRY(c, launch_pack(c->dtype, sv, mine + bk.ce_off + r * bk.ce_stride, scale, (int)c->pack_ctas, c->comm));
+  prof_end(c);
+  CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->comm));
+  prof_begin(c, 4);
+  for (int i = 1; i < W; ++i) {
+    const int j = (r + i) % W;
+    CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->storage[j]) + bk.ce_off + r * bk.ce_stride,
+                                mine + bk.ce_off + r * bk.ce_stride, bytes, cudaMemcpyDeviceToDevice, c->comm));
+  }
+  prof_end(c);
+  for (int i = 1; i < W; ++i) {
+    const int j = (r + i) % W;
+    if (ddp_status_t st = ce_write(c, c->comm, ce_flag(c, j, 0, b, r), v)) return st;
+  }
+  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_red, c->ce_packed[b], 0));
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_wait(c, c->ce_red, ce_flag(c, r, 0, b, (r + i) % W), v)) return st;
+  prof_begin(c, 5, c->ce_red);
+  CUDA_TRY(c, launch_ce_reduce(c->dtype, W, sv, mine + bk.ce_off, bk.ce_stride / c->esize, (int)c->pack_ctas,
+                               c->ce_red));
+  prof_end(c, c->ce_red);
+  for (int i = 1; i < W; ++i) {
+    const int j = (r + i) % W;
+    if (ddp_status_t st = ce_write(c, c->ce_red, ce_flag(c, j, 1, b, r), v)) return st;
+  }
+  c->ce_used = true;
+  return DDP_OK;
 }
 
 // ---- a3/a4/a6 device work for one bucket -------------------------------------
@@ -267,6 +354,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   const SlotView sv{bk.off.data(), bk.grads.data(), (int32_t)bk.params.size()};
   const float scale = 1.0f / (float)c->world;  // fl(1/W), reading C-2
   char* mine = static_cast<char*>(c->storage[c->rank]);
+  if (bk.algo == DDP_ALGO_CE) return launch_ce(c, b, sv, scale);
   if (bk.algo == DDP_ALGO_NCCL) {
     void* buf = mine + bk.byte_off;
     prof_begin(c, 0);
@@ -494,6 +582,12 @@ void ddp_destroy(ddp_ctx_t* c) {
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->prof_ready) cudaEventDestroy(e);
   if (c->comm_done) cudaEventDestroy(c->comm_done);
+  if (c->ce_red) {
+    if (!c->poisoned) cudaStreamSynchronize(c->ce_red);
+    cudaStreamDestroy(c->ce_red);
+  }
+  for (cudaEvent_t e : c->ce_packed) cudaEventDestroy(e);
+  if (c->ce_red_done) cudaEventDestroy(c->ce_red_done);
   if (c->err_host) cudaFreeHost(c->err_host);
   delete c;
 }
@@ -574,6 +668,22 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
   NCCL_TRY(c, ncclCommInitRank(&c->nccl, c->world, id, c->rank));
   char* mine = static_cast<char*>(c->storage[c->rank]);
   CUDA_TRY(c, cudaMemsetAsync(mine + c->flags_off, 0, kFlagsBytes, c->comm));
+  CUDA_TRY(c, cudaMemsetAsync(mine + c->ce_flags_off, 0, (size_t)c->buckets.size() * kMaxWorld * 2 * 4, c->comm));
+  bool any_ce = false;
+  for (const Bucket& bk : c->buckets) any_ce |= bk.algo == DDP_ALGO_CE;
+  if (any_ce) {
+    int lo = 0, hi = 0;
+    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_red, cudaStreamNonBlocking, hi));
+    c->ce_packed.assign(c->buckets.size(), nullptr);
+    for (auto& e : c->ce_packed) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ce_red_done, cudaEventDisableTiming));
+    cudaDriverEntryPointQueryResult q1, q2;
+    CUDA_TRY(c, cudaGetDriverEntryPoint("cuStreamWriteValue32", &c->fn_write32, cudaEnableDefault, &q1));
+    CUDA_TRY(c, cudaGetDriverEntryPoint("cuStreamWaitValue32", &c->fn_wait32, cudaEnableDefault, &q2));
+    if (q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !c->fn_write32 || !c->fn_wait32)
+      return fail(DDP_ERR_UNSUPPORTED, "stream memory operations unavailable (copy-engine algorithm)");
+  }
   // every rank's flags are zero before anyone's first P2P launch
   NCCL_TRY(c, ncclAllReduce(mine + kBarrierScratch, mine + kBarrierScratch, 1, ncclInt32, ncclSum, c->nccl, c->comm));
   CUDA_TRY(c, cudaStreamSynchronize(c->comm));
@@ -594,7 +704,8 @@ ddp_status_t ddp_bind_emulated(ddp_ctx_t* c, int32_t device, void* comm_stream, 
       return fail(DDP_ERR_INVALID_ARG, "storages must be non-null and 256-B aligned");
   }
   for (const Bucket& bk : c->buckets)
-    if (bk.algo == DDP_ALGO_NCCL) return fail(DDP_ERR_UNSUPPORTED, "emulation runs P2P buckets only (set DDP_OPT_ALGO)");
+    if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE)
+      return fail(DDP_ERR_UNSUPPORTED, "emulation runs the one-shot / two-shot kernels only (set DDP_OPT_ALGO)");
   if (ddp_status_t st = bind_common(c, device, comm_stream)) return st;
   for (int r = 0; r < c->world; ++r) c->storage[r] = storages[r];
   c->grad_rank_stride = grad_rank_stride_bytes;
@@ -653,6 +764,11 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
     if (ddp_status_t st = launch_range(c, b0, nb, c->n_ready)) return st;
     if (!c->dry_run) {
       CUDA_TRY(c, cudaEventRecord(c->comm_done, c->comm));
+      if (c->ce_used) {  // copy-engine reductions write .grad on the reduce stream
+        CUDA_TRY(c, cudaEventRecord(c->ce_red_done, c->ce_red));
+        CUDA_TRY(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), c->ce_red_done, 0));
+        c->ce_used = false;
+      }
       CUDA_TRY(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), c->comm_done, 0));
     }
   }
@@ -699,7 +815,7 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       c->twoshot_max = v;
       break;
     case DDP_OPT_ALGO:
-      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_TWOSHOT) return fail(DDP_ERR_INVALID_ARG, "bad algo");
+      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_CE) return fail(DDP_ERR_INVALID_ARG, "bad algo");
       c->algo = v;
       break;
     case DDP_OPT_COMM_CTAS:
@@ -752,10 +868,10 @@ ddp_status_t ddp_launch_trace(const ddp_ctx_t* c, int32_t* buckets, int32_t* tri
   return DDP_OK;
 }
 
-ddp_status_t ddp_profile_read(ddp_ctx_t* c, double ms[4], int64_t launches[4]) {
+ddp_status_t ddp_profile_read(ddp_ctx_t* c, double ms[6], int64_t launches[6]) {
   if (ddp_status_t st = check_ctx(c)) return st;
   if (!ms || !launches) return fail(DDP_ERR_INVALID_ARG, "null argument");
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < 6; ++k) {
     ms[k] = 0;
     launches[k] = 0;
   }

@@ -61,6 +61,10 @@ cudaError_t launch_pack(int dtype, const SlotView& sv, void* bucket, float scale
 cudaError_t launch_unpack(int dtype, const SlotView& sv, const void* bucket, int max_ctas,
                           cudaStream_t s);
 cudaError_t launch_p2p(int algo, int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
+// Copy-engine algorithm, SM part: grad = RNE(sum over the W slots, rank order);
+// slot q of element x at slot0 + q * stride_elems + x.
+cudaError_t launch_ce_reduce(int dtype, int world, const SlotView& sv, const void* slot0, int64_t stride_elems,
+                             int max_ctas, cudaStream_t s);
 // Largest number of CTAs per rank an emulated launch of `world` ranks may use.
 int emulated_max_ctas(int algo, int dtype, int n_slots, int world);
 

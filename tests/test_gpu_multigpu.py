@@ -98,7 +98,8 @@ def test_multigpu_parity(world):
     from paper_2006_15704_b200 import _lib as L
     cfgs = [("toy", "fp32", 4096, L.ALGO_ONESHOT, 2), ("toy", "bf16", 4096, L.ALGO_TWOSHOT, 2),
             ("toy", "fp32", 4096, L.ALGO_NCCL, 1), ("resnet50", "fp32", 25 * MIB, L.ALGO_AUTO, 2),
-            ("resnet50", "bf16", 25 * MIB, L.ALGO_TWOSHOT, 1), ("resnet50", "bf16", 25 * MIB, L.ALGO_NCCL, 1)]
+            ("resnet50", "bf16", 25 * MIB, L.ALGO_TWOSHOT, 1), ("resnet50", "bf16", 25 * MIB, L.ALGO_NCCL, 1),
+            ("toy", "bf16", 4096, L.ALGO_CE, 3), ("resnet50", "fp32", 25 * MIB, L.ALGO_CE, 2)]
     outs = _run(world, cfgs)
     for ci, (model, dtype, cap, algo, iters) in enumerate(cfgs):
         ns = numels(model)
