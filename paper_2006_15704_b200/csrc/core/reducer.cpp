@@ -88,7 +88,7 @@ struct ddp_ctx {
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
           stage1_stride = 0, ce_flags_off = 0, storage_bytes = 0;
   // copy-engine path: reduce stream, events, driver stream-memory-op entry points
-  cudaStream_t ce_red = nullptr;
+  cudaStream_t ce_red = nullptr, ce_pack = nullptr;
   std::vector<cudaEvent_t> ce_packed;  // per bucket: own slot packed (comm -> reduce stream)
   cudaEvent_t ce_red_done = nullptr;
   void* fn_write32 = nullptr;
@@ -315,13 +315,17 @@ ddp_status_t launch_ce(ddp_ctx* c, int b, const SlotView& sv, float scale) {
   char* mine = static_cast<char*>(c->storage[r]);
   const uint32_t v = ++bk.ce_count;
   const int64_t bytes = bk.numel * c->esize;
+  // pack on its own stream so bucket b+1 packs while bucket b is on the copy engines
+  prof_begin(c, 0, c->ce_pack);
+  CUDA_TRY(c, launch_pack(c->dtype, sv, mine + bk.ce_off + r * bk.ce_stride, scale, (int)c->pack_ctas,
+                          c->ce_pack));
+  prof_end(c, c->ce_pack);
+  CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_packed[b], 0));
+  // reuse guard: every peer has consumed (reduced) its slot r of this bucket from pass v-1
   if (v > 1)
     for (int i = 1; i < W; ++i)
       if (ddp_status_t st = ce_wait(c, c->comm, ce_flag(c, r, 1, b, (r + i) % W), v - 1)) return st;
-  prof_begin(c, 0);
-  CUDA_TRY(c, launch_pack(c->dtype, sv, mine + bk.ce_off + r * bk.ce_stride, scale, (int)c->pack_ctas, c->comm));
-  prof_end(c);
-  CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->comm));
   prof_begin(c, 4);
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
@@ -464,6 +468,7 @@ ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
     }
     CUDA_TRY(c, cudaEventRecord(ev, s));
     CUDA_TRY(c, cudaStreamWaitEvent(c->comm, ev, 0));
+    if (c->ce_pack) CUDA_TRY(c, cudaStreamWaitEvent(c->ce_pack, ev, 0));
   }
   c->unwaited.clear();
   if (c->world == 1 && !c->emulated) {
@@ -582,9 +587,10 @@ void ddp_destroy(ddp_ctx_t* c) {
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->prof_ready) cudaEventDestroy(e);
   if (c->comm_done) cudaEventDestroy(c->comm_done);
-  if (c->ce_red) {
-    if (!c->poisoned) cudaStreamSynchronize(c->ce_red);
-    cudaStreamDestroy(c->ce_red);
+  for (cudaStream_t s : {c->ce_red, c->ce_pack}) {
+    if (!s) continue;
+    if (!c->poisoned) cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
   }
   for (cudaEvent_t e : c->ce_packed) cudaEventDestroy(e);
   if (c->ce_red_done) cudaEventDestroy(c->ce_red_done);
@@ -675,6 +681,7 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
     int lo = 0, hi = 0;
     CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_red, cudaStreamNonBlocking, hi));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_pack, cudaStreamNonBlocking, hi));
     c->ce_packed.assign(c->buckets.size(), nullptr);
     for (auto& e : c->ce_packed) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->ce_red_done, cudaEventDisableTiming));
