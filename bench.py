@@ -41,7 +41,7 @@ MIB = 1 << 20
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="resnet50", choices=["resnet50", "bert_large"])
@@ -80,30 +80,61 @@ def measured_peaks():
     return 6650.0, "fallback"
 
 
-class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+def ncu_traffic(workload, world, kind):
+    """DRAM bytes per launch of the dominant kernel from a committed ncu --set full
+    capture (profiles/traffic.json), or (None, None) when none matches."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            e = json.load(f).get(f"{workload}|W{world}|{kind}")
+    except (OSError, ValueError):
+        e = None
+    return (e["bytes"], e["source"]) if e else (None, None)
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+class ClockSampler:
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML polled
+    every ~2 ms from a thread (nvidia-smi as a fallback when NVML is missing)."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index, self.samples, self._stop = index, [], threading.Event()
         self.t = threading.Thread(target=self._run, daemon=True)
+        self.src = "nvml"
 
     def _run(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                    N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append([sm, mx] + [bool(rs & b) for b in bits])
+                self._stop.wait(0.002)
+            return
+        except Exception:
+            self.src = "nvidia-smi"
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
+                x = [v.strip() for v in out.split(",")]
+                self.samples.append([float(x[0]), float(x[1])] + [v == "Active" for v in x[2:6]])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.05)
 
     def __enter__(self):
         self.t.start()
+        time.sleep(0.01)
         return self
 
     def __exit__(self, *exc):
@@ -112,14 +143,12 @@ class ClockSampler:
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         import statistics
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+        reasons = sorted({self.NAMES[i] for s in self.samples for i in range(4) if s[2 + i]})
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples), "reasons": reasons,
+                "samples": len(self.samples), "source": self.src}
 
 
 # ---------------------------------------------------------------------------------
@@ -282,7 +311,7 @@ def run_ours(a):
         peak = peak_hbm if bound == "hbm" else 770.0
         roof = {"bound": bound, "achieved": byts / (avg_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s"}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"] = None
+        roof["traffic"], roof["traffic_source"] = ncu_traffic(workload_name(a), world, dom)
         roof["kernel"] = dom
         roof["algorithmic_bytes_per_launch"] = byts
         roof["bytes_rule"] = per
