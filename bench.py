@@ -60,6 +60,12 @@ def parse():
     ap.add_argument("--timeline-detail", action="store_true", help="include per-launch timeline in the JSON")
     ap.add_argument("--oneshot-max", type=int, default=-1)
     ap.add_argument("--twoshot-max", type=int, default=-1)
+    ap.add_argument("--mode", default="step", choices=["step", "cap-sweep", "nosync", "allreduce-sweep"],
+                    help="step: the contract line (default).  cap-sweep: BASELINE config 4 (exposed time vs "
+                         "bucket cap, real model).  nosync: config 5 (sync every 1/2/4/8).  allreduce-sweep: "
+                         "M-3 per-size busBW per algorithm + the paper's fixed-total split (Fig. 2 method)")
+    ap.add_argument("--exposed-seq", type=int, default=0, help="BERT sequence length (default 512)")
+    ap.add_argument("--caps", default="0,1,5,10,25,50,100,200", help="cap-sweep caps in MiB")
     return ap.parse_args()
 
 
@@ -410,52 +416,62 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
-def measure_exposed(a, rank, world, local, dev, opts):
-    """Exposed (non-overlapped) sync time with a REAL backward (SURVEY §8(d) M-2):
-    the DDP front end's post-accumulate hooks drive the library during
-    loss.backward() of a randomly initialised model on synthetic data.
-    T_sync: event before backward() -> event after it returns (the finalize
-    callback has made the stream wait for the comm stream).  T_bwd: the same
-    window inside no_sync (hooks still fire and return early).  Interleaved
-    pairs; exposed = median(T_sync) - median(T_bwd), max over ranks."""
-    import statistics
-
+def build_model(name, dtype, batch, seq, rank, dev):
+    """A randomly initialised model of the paper's families on synthetic data:
+    torchvision ResNet-50 (224x224 images, CrossEntropy as in P:L329) or HF
+    BertModel-large (random token ids).  Returns (model, loss_fn, description)."""
     import torch
-    import torch.distributed as dist
-    from paper_2006_15704_b200.ddp import DistributedDataParallel
 
     torch.backends.cudnn.benchmark = True
     torch.backends.cuda.matmul.allow_tf32 = True
     torch.backends.cudnn.allow_tf32 = True
     g = torch.Generator(device=dev).manual_seed(15704 + rank)
-    if a.exposed_model == "resnet50":
+    if name == "resnet50":
         import torchvision
         model = torchvision.models.resnet50().to(dev)
-        B = a.exposed_batch or 64
+        B = batch or 64
         x = torch.randn(B, 3, 224, 224, device=dev, generator=g)
         y = torch.randint(0, 1000, (B,), device=dev, generator=g)
+        if dtype == "bf16":
+            model, x = model.to(torch.bfloat16), x.to(torch.bfloat16)
         lossf = torch.nn.CrossEntropyLoss()
 
         def fwd(m):
             return lossf(m(x), y)
-        desc = f"torchvision resnet50, batch {B}/GPU, 224x224, CrossEntropy"
-    else:
-        import transformers
-        cfg = transformers.BertConfig(hidden_size=1024, num_hidden_layers=24, num_attention_heads=16,
-                                      intermediate_size=4096)
-        model = transformers.BertModel(cfg).to(dev)
-        B, S = (a.exposed_batch or 8), 512
-        ids = torch.randint(0, cfg.vocab_size, (B, S), device=dev, generator=g)
-
-        def fwd(m):  # touches every parameter (pooler included): no unused parameters
-            o = m(input_ids=ids)
-            return o.last_hidden_state.float().pow(2).mean() + o.pooler_output.float().pow(2).mean()
-        desc = f"HF BertModel-large, {B}x{S} tokens/GPU, mean-square loss on hidden states + pooler"
-    if a.dtype == "bf16":
+        return model, fwd, f"torchvision resnet50, batch {B}/GPU, 224x224, CrossEntropy"
+    import transformers
+    cfg = transformers.BertConfig(hidden_size=1024, num_hidden_layers=24, num_attention_heads=16,
+                                  intermediate_size=4096)
+    model = transformers.BertModel(cfg).to(dev)
+    if dtype == "bf16":
         model = model.to(torch.bfloat16)
-        if a.exposed_model == "resnet50":
-            x = x.to(torch.bfloat16)
-    ddp = DistributedDataParallel(model, bucket_cap_mb=a.cap_mib, options=opts)
+    B, S = (batch or 8), (seq or 512)
+    ids = torch.randint(0, cfg.vocab_size, (B, S), device=dev, generator=g)
+
+    def fwd(m):  # touches every parameter (pooler included): no unused parameters
+        o = m(input_ids=ids)
+        return o.last_hidden_state.float().pow(2).mean() + o.pooler_output.float().pow(2).mean()
+    return model, fwd, f"HF BertModel-large, {B}x{S} tokens/GPU, mean-square loss on hidden states + pooler"
+
+
+def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev, dtype,
+                timeline_detail=False, nosync_every=(), no_overlap=True):
+    """Exposed (non-overlapped) sync time with a REAL backward (SURVEY §8(d) M-2):
+    the DDP front end's post-accumulate hooks drive the library during
+    loss.backward().  T_sync: event before backward() -> event after it returns
+    (the finalize callback has made the stream wait for the comm stream).
+    T_bwd: the same window inside no_sync (hooks still fire and return early).
+    Interleaved; exposed = median(T_sync) - median(T_bwd), max over ranks.
+    nosync_every: for each n, groups of n-1 no_sync passes + 1 synced pass
+    (config 5): amortized ms/iter of the group and exposed/iter."""
+    import statistics
+
+    import torch
+    import torch.distributed as dist
+    from paper_2006_15704_b200 import _lib as L
+    from paper_2006_15704_b200.ddp import DistributedDataParallel
+
+    ddp = DistributedDataParallel(model, bucket_cap_mb=cap_mib, options=opts)
     stream = torch.cuda.current_stream(dev)
 
     def one(sync: bool) -> float:
@@ -475,19 +491,45 @@ def measure_exposed(a, rank, world, local, dev, opts):
         torch.cuda.synchronize(dev)
         return s.elapsed_time(e)
 
+    def group(n: int) -> float:
+        """n-1 accumulating no_sync backward passes + 1 synced one: summed backward ms."""
+        for p in ddp.params:
+            p.grad = None
+        tot = 0.0
+        for k in range(n):
+            loss = fwd(ddp)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if k < n - 1:
+                with ddp.no_sync():
+                    s.record(stream)
+                    loss.backward()
+                    e.record(stream)
+            else:
+                s.record(stream)
+                loss.backward()
+                e.record(stream)
+            torch.cuda.synchronize(dev)
+            tot += s.elapsed_time(e)
+        return tot
+
     for _ in range(3):
         one(True)
         one(False)
     if world > 1:
         dist.barrier(device_ids=[local])
-    from paper_2006_15704_b200 import _lib as L
     ts, tb, tn = [], [], []
-    for _ in range(a.exposed_iters):
+    for _ in range(iters):
         ts.append(one(True))
         tb.append(one(False))
-        ddp.reducer.set_option(L.OPT_OVERLAP, 0)   # paper's non-overlapped baseline
-        tn.append(one(True))
-        ddp.reducer.set_option(L.OPT_OVERLAP, 1)
+        if no_overlap:
+            ddp.reducer.set_option(L.OPT_OVERLAP, 0)   # paper's non-overlapped baseline (P:L399)
+            tn.append(one(True))
+            ddp.reducer.set_option(L.OPT_OVERLAP, 1)
+    ns_res = {}
+    for n in nosync_every:
+        group(n)
+        gt = [group(n) for _ in range(max(2, iters // 2))]
+        ns_res[n] = statistics.median(gt)
     # one profiled synced pass: Fig. 2(c)-style ready / start / end timeline of the comm launches
     ddp.reducer.set_option(L.OPT_PROFILE, 1)
     L.ddp_profile_timeline(ddp.reducer.ctx)
@@ -502,23 +544,176 @@ def measure_exposed(a, rank, world, local, dev, opts):
                     "max_queue_delay_ms": max(s - r for _, r, s, _ in tl),
                     "comm_busy_ms": sum(e - s for _, _, s, e in tl),
                     "per_launch": [[k, round(r, 4), round(s, 4), round(e, 4)] for k, r, s, e in tl]
-                    if a.timeline_detail else None}
+                    if timeline_detail else None}
     ddp.reducer.check_errors()
-    vals = torch.tensor([statistics.median(ts), statistics.median(tb), statistics.median(tn)],
-                        dtype=torch.float64, device=dev)
+    vals = [statistics.median(ts), statistics.median(tb), statistics.median(tn) if tn else 0.0]
+    vals += [ns_res[n] for n in nosync_every]
+    vt = torch.tensor(vals, dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-    t_sync, t_bwd, t_noov = float(vals[0]), float(vals[1]), float(vals[2])
-    res = {"model": desc, "dtype": a.dtype, "bucket_cap_mib": a.cap_mib,
+        dist.all_reduce(vt, op=dist.ReduceOp.MAX)
+    t_sync, t_bwd, t_noov = float(vt[0]), float(vt[1]), float(vt[2])
+    res = {"model": desc, "dtype": dtype, "bucket_cap_mib": cap_mib,
            "buckets": ddp.reducer.num_buckets, "bucket_algos": ddp.reducer.bucket_algos(),
            "t_bwd_ms": t_bwd, "t_bwd_plus_sync_ms": t_sync, "exposed_ms": t_sync - t_bwd,
            "exposed_pct_of_bwd": 100.0 * (t_sync - t_bwd) / t_bwd,
-           "t_bwd_plus_sync_no_overlap_ms": t_noov, "exposed_no_overlap_ms": t_noov - t_bwd,
-           "iters": a.exposed_iters, "timing": "median of interleaved triples, max over ranks",
+           "iters": iters, "timing": "median of interleaved passes, max over ranks",
            "timeline_rank0": timeline if rank == 0 else None}
-    ddp.reducer.close()
-    del ddp, model
+    if no_overlap:
+        res["t_bwd_plus_sync_no_overlap_ms"] = t_noov
+        res["exposed_no_overlap_ms"] = t_noov - t_bwd
+    if nosync_every:
+        res["nosync"] = {str(n): {"ms_per_iter": float(vt[3 + i]) / n,
+                                  "exposed_ms_per_iter": (float(vt[3 + i]) - n * t_bwd) / n}
+                         for i, n in enumerate(nosync_every)}
+    ddp.close()
+    return res
+
+
+def measure_exposed(a, rank, world, local, dev, opts):
+    import torch
+    model, fwd, desc = build_model(a.exposed_model, a.dtype, a.exposed_batch, 0, rank, dev)
+    res = exposed_for(model, fwd, desc, a.cap_mib, opts, a.exposed_iters, rank, world, local, dev, a.dtype,
+                      a.timeline_detail)
+    del model
     torch.cuda.empty_cache()
+    return res
+
+
+def _init_dist(a):
+    import torch
+    import torch.distributed as dist
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    return rank, world, local, dev
+
+
+def _opts(a):
+    from paper_2006_15704_b200 import _lib as L
+    o = {}
+    for key, v in ((L.OPT_ALGO, a.algo), (L.OPT_COMM_CTAS, a.comm_ctas), (L.OPT_PACK_CTAS, a.pack_ctas)):
+        if v:
+            o[key] = v
+    if a.stage_kib:
+        o[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
+    if a.oneshot_max >= 0:
+        o[L.OPT_P2P_ONESHOT_MAX] = a.oneshot_max
+    if a.twoshot_max >= 0:
+        o[L.OPT_P2P_TWOSHOT_MAX] = a.twoshot_max
+    return o
+
+
+def run_sweep(a):
+    """Secondary measurements (one JSON line per point, rank 0), SURVEY §8(d) M-1/M-3."""
+    import torch
+    import torch.distributed as dist
+    rank, world, local, dev = _init_dist(a)
+    opts = _opts(a)
+    out = []
+    if a.mode in ("cap-sweep", "nosync"):
+        name = a.exposed_model if a.exposed_model != "none" else a.workload
+        model, fwd, desc = build_model(name, a.dtype, a.exposed_batch, a.exposed_seq, rank, dev)
+        if a.mode == "cap-sweep":
+            for cap in [float(c) for c in a.caps.split(",")]:
+                r = exposed_for(model, fwd, desc, cap, opts, a.exposed_iters, rank, world, local, dev, a.dtype)
+                r.update(mode="cap-sweep", n_gpus=world)
+                out.append(r)
+        else:
+            r = exposed_for(model, fwd, desc, a.cap_mib, opts, a.exposed_iters, rank, world, local, dev, a.dtype,
+                            nosync_every=(1, 2, 4, 8), no_overlap=False)
+            r.update(mode="nosync", n_gpus=world)
+            out.append(r)
+    else:
+        out = allreduce_sweep(a, rank, world, local, dev, opts)
+    if rank == 0:
+        for r in out:
+            print(json.dumps(r), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def allreduce_sweep(a, rank, world, local, dev, opts):
+    """M-3 (paper Fig. 2 method): (i) one bucket of S bytes, whole sync
+    (pack x1/W + allreduce + unpack / fused kernel) per algorithm, busBW =
+    (S/t) 2(W-1)/W; (ii) a fixed total of 60M fp32 parameters split into k equal
+    buckets (cap 0: one bucket per gradient), all launched back to back, one wait."""
+    import torch
+    import torch.distributed as dist
+    from paper_2006_15704_b200 import _lib as L
+    from paper_2006_15704_b200.ddp import GradReducer
+    from synth import device as sdev
+
+    tdt = torch.float32 if a.dtype == "fp32" else torch.bfloat16
+    esize = 4 if a.dtype == "fp32" else 2
+    stream = torch.cuda.current_stream(dev)
+    algos = [L.ALGO_AUTO, L.ALGO_NCCL, L.ALGO_ONESHOT, L.ALGO_TWOSHOT] + ([L.ALGO_CE] if world > 1 else [])
+    sizes = [4 << 10, 64 << 10, 256 << 10, 1 << 20, 4 << 20, 16 << 20, 25 << 20, 64 << 20, 256 << 20]
+    res = []
+
+    def tmax(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def time_it(fn, reps):
+        for _ in range(3):
+            fn()
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize(dev)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        for _ in range(reps):
+            fn()
+        e.record(stream)
+        torch.cuda.synchronize(dev)
+        return tmax(s.elapsed_time(e) / reps)
+
+    for S in sizes:
+        n = S // esize
+        g = torch.empty(n, dtype=tdt, device=dev)
+        sdev.fill(g, 15704, rank, 0, 0, "normal", a.dtype)
+        for algo in algos:
+            o = dict(opts)
+            o[L.OPT_ALGO] = algo
+            red = GradReducer([n], a.dtype, S, options=o)
+
+            def one():
+                red.grad_ready(0, g, stream)
+                red.finalize(stream)
+            t = time_it(one, 20 if S <= (64 << 20) else 5)
+            bw = S / (t * 1e-3) * 2 * (world - 1) / world / 1e9 if world > 1 else None
+            res.append({"mode": "allreduce-sweep", "n_gpus": world, "dtype": a.dtype, "bytes": S,
+                        "algo": red.bucket_algos()[0], "forced": L.ALGO_NAMES[algo] if algo else "auto",
+                        "ms": t, "busbw_gbs": bw, "algbw_gbs": S / (t * 1e-3) / 1e9,
+                        "includes": "pack x1/W + allreduce + unpack (fused kernel for P2P)"})
+            red.close()
+        del g
+    # (ii) fixed total, k equal gradients, cap 0 (one bucket per gradient), one batched ready call
+    total = 60_000_000 if a.dtype == "fp32" else 60_000_000
+    for per in (1_000, 10_000, 100_000, 1_000_000, 10_000_000, 60_000_000):
+        k = total // per
+        flat = torch.empty(k * per, dtype=tdt, device=dev)
+        sdev.fill(flat, 15704, rank, 0, 1, "normal", a.dtype)
+        for algo in (L.ALGO_AUTO, L.ALGO_NCCL):
+            o = dict(opts)
+            o[L.OPT_ALGO] = algo
+            red = GradReducer([per] * k, a.dtype, 0, options=o)
+            batch = L.ReadyBatch(list(range(k - 1, -1, -1)),
+                                 [flat[p * per:].data_ptr() for p in range(k - 1, -1, -1)])
+
+            def one():
+                red.grads_ready(batch, stream)
+                red.finalize(stream)
+            t = time_it(one, 3)
+            res.append({"mode": "fixed-total-split", "n_gpus": world, "dtype": a.dtype, "total_params": k * per,
+                        "params_per_op": per, "ops": k, "algo": red.bucket_algos()[0],
+                        "forced": L.ALGO_NAMES[algo] if algo else "auto", "ms_total": t})
+            red.close()
+        del flat
     return res
 
 
@@ -526,8 +721,10 @@ def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
-    else:
+    elif a.mode == "step":
         run_ours(a)
+    else:
+        run_sweep(a)
 
 
 if __name__ == "__main__":

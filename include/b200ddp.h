@@ -76,8 +76,12 @@ enum {
   DDP_OPT_ALGO = 7,             /* force the bucket allreduce: 0 auto, 1 NCCL, 2 one-shot, 3 two-shot,
                                    4 copy-engine one-shot (world > 1) */
   DDP_OPT_PACK_CTAS = 8,        /* max CTAs of pack/unpack kernels and of P2P kernels at world 1 */
-  DDP_OPT_P2P_STAGE_BYTES = 9   /* 0 (default): one pipeline stage per CTA chunk; else split each
+  DDP_OPT_P2P_STAGE_BYTES = 9,  /* 0 (default): one pipeline stage per CTA chunk; else split each
                                    CTA chunk into stages of this many bytes (one sync per stage) */
+  DDP_OPT_FIND_UNUSED = 10      /* 1: globally-unused-parameter detection:
+                                   enables ddp_mark_unused, a participation bitmap and one extra
+                                   allreduce per synced pass; CREATED only (storage grows by one
+                                   bucket-region-sized scratch + the bitmap) */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.
@@ -146,6 +150,28 @@ ddp_status_t ddp_grad_ready(ddp_ctx_t* ctx, int32_t param_idx, void* grad, void*
 /* Batched form: equivalent to n successive ddp_grad_ready calls in array order. */
 ddp_status_t ddp_grads_ready(ddp_ctx_t* ctx, int32_t n, const int32_t* param_idx,
                              void* const* grads, void* producer_stream);
+/* ddp_mark_unused: Alg. 1 forward (L224-L225) "traverse autograd graph from out
+ * and mark unused parameters as ready": param_idx will get no gradient in this
+ * pass.  Counts as its ready signal (buckets holding it can launch without
+ * waiting).  Requires DDP_OPT_FIND_UNUSED.
+ *   grad: param_idx's current gradient buffer, or NULL if it has none.  If the
+ *   parameter got a gradient in an earlier no_sync pass since the last synced
+ *   pass (so it participates), grad must be that accumulated gradient
+ *   and it is synchronized like any other.  Otherwise its local contribution is
+ *   zero (P:L310 local bitmap); after the pass's extra bitmap allreduce the
+ *   average is written into grad (if non-NULL) only when some rank used the
+ *   parameter; a parameter unused on every rank keeps its gradient intact
+ *   ("DDP should only touch gradients that are indeed involved").
+ *   producer_stream: orders the library's zero-fill of the local contribution.
+ * Errors: as ddp_grad_ready; DDP_ERR_STATE if FIND_UNUSED is off;
+ * DDP_ERR_INVALID_ARG if grad is NULL for a participating parameter. */
+ddp_status_t ddp_mark_unused(ddp_ctx_t* ctx, int32_t param_idx, void* grad, void* producer_stream);
+/* ddp_global_unused: after the finalize of a synced pass with FIND_UNUSED, blocks
+ * the host until that pass's bitmap allreduce has completed and writes
+ * out[p] = 1 if parameter p was unused on every rank (its gradient was left
+ * untouched), else 0, for p < n (n <= number of parameters).
+ * Errors: DDP_ERR_STATE if no synced FIND_UNUSED pass has finished. */
+ddp_status_t ddp_global_unused(ddp_ctx_t* ctx, uint8_t* out, int32_t n);
 /* ddp_finalize_backward: closes the pass ("block waiting for all
  * AllReduce ops", done asynchronously: the consumer stream waits on the comm
  * stream, no host block).  Launches any deferred buckets (OVERLAP=0) and

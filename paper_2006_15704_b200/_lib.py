@@ -23,7 +23,7 @@ STATUS_NAMES = ["OK", "INVALID_ARG", "STATE", "DUPLICATE", "INCOMPLETE", "CUDA",
                 "POISONED", "TIMEOUT", "UNSUPPORTED"]
 FP32, BF16 = 0, 1
 OPT_OVERLAP, OPT_P2P_ONESHOT_MAX, OPT_P2P_TWOSHOT_MAX, OPT_COMM_CTAS, OPT_DRY_RUN, OPT_PROFILE, \
-    OPT_ALGO, OPT_PACK_CTAS, OPT_P2P_STAGE_BYTES = range(1, 10)
+    OPT_ALGO, OPT_PACK_CTAS, OPT_P2P_STAGE_BYTES, OPT_FIND_UNUSED = range(1, 11)
 ALGO_AUTO, ALGO_NCCL, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_CE = range(5)
 ALGO_NAMES = {ALGO_NCCL: "nccl", ALGO_ONESHOT: "oneshot", ALGO_TWOSHOT: "twoshot", ALGO_CE: "ce"}
 PROFILE_KINDS = ("pack", "nccl_allreduce", "unpack", "p2p_fused", "ce_copy", "ce_reduce")
@@ -54,6 +54,8 @@ _SIGS = {
     "ddp_grad_ready": (C.c_int, [_P, C.c_int32, _P, _P]),
     "ddp_grads_ready": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(_P), _P]),
     "ddp_finalize_backward": (C.c_int, [_P, _P]),
+    "ddp_mark_unused": (C.c_int, [_P, C.c_int32, _P, _P]),
+    "ddp_global_unused": (C.c_int, [_P, C.POINTER(C.c_uint8), C.c_int32]),
     "ddp_no_sync_begin": (C.c_int, [_P]),
     "ddp_no_sync_end": (C.c_int, [_P]),
     "ddp_set_option": (C.c_int, [_P, C.c_int32, C.c_int64]),
@@ -173,6 +175,16 @@ def ddp_grads_ready(ctx: int, batch: ReadyBatch, producer_stream: int) -> None:
 
 def ddp_finalize_backward(ctx: int, consumer_stream: int) -> None:
     _check(lib().ddp_finalize_backward(ctx, consumer_stream))
+
+
+def ddp_mark_unused(ctx: int, param_idx: int, grad_ptr: int, producer_stream: int) -> None:
+    _check(lib().ddp_mark_unused(ctx, param_idx, grad_ptr or None, producer_stream))
+
+
+def ddp_global_unused(ctx: int, n: int) -> List[bool]:
+    out = (C.c_uint8 * max(1, n))()
+    _check(lib().ddp_global_unused(ctx, out, n))
+    return [bool(out[i]) for i in range(n)]
 
 
 def ddp_no_sync_begin(ctx: int) -> None:

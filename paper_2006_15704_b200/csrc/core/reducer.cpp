@@ -83,10 +83,22 @@ struct ddp_ctx {
   // oneshot_max < 0: automatic (world 2: every bucket one-shot — it sends the same
   // NVLink bytes as two-shot with one sync instead of two; world > 2: <= 512 KiB)
   int64_t overlap = 1, oneshot_max = -1, twoshot_max = INT64_MAX, comm_ctas = 64,
-          dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 8, stage_bytes = 0;
+          dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 8, stage_bytes = 0,
+          find_unused = 0;
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
-          stage1_stride = 0, ce_flags_off = 0, storage_bytes = 0;
+          stage1_stride = 0, ce_flags_off = 0, bitmap_off = 0, scratch_off = 0, storage_bytes = 0;
+  // find_unused: local participation since the last
+  // synced pass, this pass's locally-unused parameters and their destinations
+  std::vector<uint8_t> used_local;
+  std::vector<int32_t> un_param;
+  std::vector<void*> un_dst;
+  std::vector<const void*> un_src;
+  std::vector<int64_t> un_numel;
+  int32_t* bitmap_host = nullptr;   // pinned: local bitmap (H2D source)
+  int32_t* global_host = nullptr;   // pinned: summed bitmap (D2H target)
+  cudaEvent_t bitmap_done = nullptr;
+  bool bitmap_valid = false;
   // copy-engine path: reduce stream, events, driver stream-memory-op entry points
   cudaStream_t ce_red = nullptr, ce_pack = nullptr;
   std::vector<cudaEvent_t> ce_packed;  // per bucket: own slot packed (comm -> reduce stream)
@@ -246,6 +258,15 @@ void plan(ddp_ctx* c) {
     bk.ce_stride = align_up(bk.numel * c->esize, 256);
     bk.ce_off = pos;
     pos += c->world * bk.ce_stride;
+  }
+  // find_unused: device bitmap (int32 per param) + a scratch copy of the bucket region
+  // (locally-unused parameters pack zeros from, and receive the average into, it)
+  c->bitmap_off = c->scratch_off = 0;
+  if (c->find_unused) {
+    c->bitmap_off = pos;
+    pos += align_up((int64_t)c->numel.size() * 4, 256);
+    c->scratch_off = pos;
+    pos += c->stage2_off - c->buckets_off;
   }
   c->storage_bytes = pos;
   for (Bucket& bk : c->buckets) grid_for(c, bk, max_ctas_for(c, bk));
@@ -503,18 +524,79 @@ void open_pass(ddp_ctx* c) {
   c->cursor = 0;
   c->n_ready = 0;
   c->trace.clear();
+  c->un_param.clear();
+  c->un_dst.clear();
+  c->un_src.clear();
+  c->un_numel.clear();
 }
 
-ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s) {
+// find_unused, end of a synced pass: local bitmap -> device (non-blocking
+// copy from pinned host memory), ONE extra allreduce (sum) of the bitmap on the
+// comm stream after every bucket, write-back of the locally-unused parameters
+// that some rank used, and the summed bitmap back to the host for
+// ddp_global_unused.  Then the local bitmap restarts (next synced window).
+ddp_status_t finish_unused(ddp_ctx* c) {
+  const int32_t n = (int32_t)c->numel.size();
+  if (c->bitmap_valid) CUDA_TRY(c, cudaEventSynchronize(c->bitmap_done));  // host buffers reusable
+  for (int32_t p = 0; p < n; ++p) c->bitmap_host[p] = c->used_local[p];
+  int32_t* dev_bitmap = reinterpret_cast<int32_t*>(static_cast<char*>(c->storage[c->rank]) + c->bitmap_off);
+  CUDA_TRY(c, cudaMemcpyAsync(dev_bitmap, c->bitmap_host, (size_t)n * 4, cudaMemcpyHostToDevice, c->comm));
+  NCCL_TRY(c, ncclAllReduce(dev_bitmap, dev_bitmap, (size_t)n, ncclInt32, ncclSum, c->nccl, c->comm));
+  std::vector<const void*> src;
+  std::vector<void*> dst;
+  std::vector<int32_t> prm;
+  std::vector<int64_t> cnt;
+  for (size_t k = 0; k < c->un_param.size(); ++k) {
+    if (!c->un_dst[k]) continue;  // no gradient buffer: nothing to write back
+    src.push_back(c->un_src[k]);
+    dst.push_back(c->un_dst[k]);
+    prm.push_back(c->un_param[k]);
+    cnt.push_back(c->un_numel[k]);
+  }
+  const UnusedView uv{src.data(), dst.data(), prm.data(), cnt.data(), (int32_t)src.size()};
+  CUDA_TRY(c, launch_unused_fixup(c->dtype, uv, dev_bitmap, (int)c->pack_ctas, c->comm));
+  CUDA_TRY(c, cudaMemcpyAsync(c->global_host, dev_bitmap, (size_t)n * 4, cudaMemcpyDeviceToHost, c->comm));
+  CUDA_TRY(c, cudaEventRecord(c->bitmap_done, c->comm));
+  c->bitmap_valid = true;
+  std::fill(c->used_local.begin(), c->used_local.end(), 0);
+  return DDP_OK;
+}
+
+// Scratch slot of parameter p (find_unused): mirrors its bucket position.
+char* scratch_of(ddp_ctx* c, int32_t p) {
+  const Bucket& bk = c->buckets[c->p_bucket[p]];
+  return static_cast<char*>(c->storage[c->rank]) + c->scratch_off + (bk.byte_off - c->buckets_off) +
+         c->p_off[p] * c->esize;
+}
+
+// One ready signal (a2).  unused: ddp_mark_unused (Alg. 1 forward L224-L225).
+ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s, bool unused = false) {
   if (p < 0 || p >= (int32_t)c->numel.size()) return fail(DDP_ERR_INVALID_ARG, "param index out of range");
-  if (!grad && !c->dry_run) return fail(DDP_ERR_INVALID_ARG, "null gradient pointer");
+  if (!unused && !grad && !c->dry_run) return fail(DDP_ERR_INVALID_ARG, "null gradient pointer");
+  if (unused && !c->find_unused) return fail(DDP_ERR_STATE, "ddp_mark_unused needs DDP_OPT_FIND_UNUSED");
+  if (unused && !grad && c->used_local[p] && !c->dry_run)
+    return fail(DDP_ERR_INVALID_ARG, "param " + std::to_string(p) +
+                                         " has an accumulated gradient from a no_sync pass: pass it");
   if (c->state != State::IN_PASS) open_pass(c);
   if (c->ready[p]) return fail(DDP_ERR_DUPLICATE, "param " + std::to_string(p) + " marked ready twice");
   c->ready[p] = 1;
   const int32_t t = c->n_ready++;
   const int32_t b = c->p_bucket[p];
-  c->buckets[b].grads[c->p_slot[p]] = grad;
   c->pending[b] -= 1;  // P:L306 pending count
+  if (!unused) c->used_local[p] = 1;  // participation bitmap, accumulated across no_sync
+  void* src = grad;
+  if (unused && !c->used_local[p] && !c->pass_no_sync) {
+    // no local contribution: the slot packs zeros from scratch and receives the average there
+    src = c->dry_run ? nullptr : scratch_of(c, p);
+    if (!c->dry_run) {
+      CUDA_TRY(c, cudaMemsetAsync(src, 0, (size_t)(c->numel[p] * c->esize), s));
+      c->un_param.push_back(p);
+      c->un_dst.push_back(grad);
+      c->un_src.push_back(src);
+      c->un_numel.push_back(c->numel[p]);
+    }
+  }
+  c->buckets[b].grads[c->p_slot[p]] = src;
   if (c->pass_no_sync) return DDP_OK;  // hooks disabled
   if (std::find(c->unwaited.begin(), c->unwaited.end(), s) == c->unwaited.end()) c->unwaited.push_back(s);
   if (!c->overlap) return DDP_OK;
@@ -527,7 +609,8 @@ ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s) {
 }
 
 bool is_layout_key(int32_t k) {
-  return k == DDP_OPT_P2P_ONESHOT_MAX || k == DDP_OPT_P2P_TWOSHOT_MAX || k == DDP_OPT_ALGO;
+  return k == DDP_OPT_P2P_ONESHOT_MAX || k == DDP_OPT_P2P_TWOSHOT_MAX || k == DDP_OPT_ALGO ||
+         k == DDP_OPT_FIND_UNUSED;
 }
 
 }  // namespace
@@ -558,6 +641,7 @@ ddp_status_t ddp_create(const int64_t* param_numel, int32_t n_params, int32_t dt
     c->numel.assign(param_numel, param_numel + n_params);
     assign(c);
     c->ready.assign(n_params, 0);
+    c->used_local.assign(n_params, 0);
     c->pending.assign(c->buckets.size(), 0);
     plan(c);
   } catch (const std::bad_alloc&) {
@@ -595,6 +679,9 @@ void ddp_destroy(ddp_ctx_t* c) {
   for (cudaEvent_t e : c->ce_packed) cudaEventDestroy(e);
   if (c->ce_red_done) cudaEventDestroy(c->ce_red_done);
   if (c->err_host) cudaFreeHost(c->err_host);
+  if (c->bitmap_host) cudaFreeHost(c->bitmap_host);
+  if (c->global_host) cudaFreeHost(c->global_host);
+  if (c->bitmap_done) cudaEventDestroy(c->bitmap_done);
   delete c;
 }
 
@@ -653,6 +740,12 @@ static ddp_status_t bind_common(ddp_ctx* c, int32_t device, void* comm_stream) {
   *c->err_host = 0;
   CUDA_TRY(c, cudaHostGetDevicePointer(reinterpret_cast<void**>(&c->err_dev), c->err_host, 0));
   CUDA_TRY(c, cudaEventCreateWithFlags(&c->comm_done, cudaEventDisableTiming));
+  if (c->find_unused) {
+    const size_t nb = c->numel.size() * sizeof(int32_t);
+    CUDA_TRY(c, cudaHostAlloc(reinterpret_cast<void**>(&c->bitmap_host), nb, cudaHostAllocDefault));
+    CUDA_TRY(c, cudaHostAlloc(reinterpret_cast<void**>(&c->global_host), nb, cudaHostAllocDefault));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->bitmap_done, cudaEventDisableTiming));
+  }
   return DDP_OK;
 }
 
@@ -713,6 +806,7 @@ ddp_status_t ddp_bind_emulated(ddp_ctx_t* c, int32_t device, void* comm_stream, 
   for (const Bucket& bk : c->buckets)
     if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE)
       return fail(DDP_ERR_UNSUPPORTED, "emulation runs the one-shot / two-shot kernels only (set DDP_OPT_ALGO)");
+  if (c->find_unused) return fail(DDP_ERR_UNSUPPORTED, "find_unused needs a real communicator (no emulation)");
   if (ddp_status_t st = bind_common(c, device, comm_stream)) return st;
   for (int r = 0; r < c->world; ++r) c->storage[r] = storages[r];
   c->grad_rank_stride = grad_rank_stride_bytes;
@@ -754,6 +848,21 @@ ddp_status_t ddp_grads_ready(ddp_ctx_t* c, int32_t n, const int32_t* params, voi
   return st2;
 }
 
+ddp_status_t ddp_mark_unused(ddp_ctx_t* c, int32_t p, void* grad, void* producer_stream) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (!c->bound && !c->dry_run) return fail(DDP_ERR_STATE, "context not bound to a device");
+  return grad_ready_one(c, p, grad, static_cast<cudaStream_t>(producer_stream), true);
+}
+
+ddp_status_t ddp_global_unused(ddp_ctx_t* c, uint8_t* out, int32_t n) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (!out || n < 0 || n > (int32_t)c->numel.size()) return fail(DDP_ERR_INVALID_ARG, "bad output");
+  if (!c->bitmap_valid) return fail(DDP_ERR_STATE, "no synced find_unused pass has finished");
+  CUDA_TRY(c, cudaEventSynchronize(c->bitmap_done));
+  for (int32_t p = 0; p < n; ++p) out[p] = c->global_host[p] == 0 ? 1 : 0;
+  return DDP_OK;
+}
+
 ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
   if (ddp_status_t st = check_ctx(c)) return st;
   if (c->state != State::IN_PASS) return fail(DDP_ERR_STATE, "no backward pass is open");
@@ -769,6 +878,13 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
     const int32_t b0 = c->cursor;  // OVERLAP=0: all launches at finalize, in order
     c->cursor = nb;
     if (ddp_status_t st = launch_range(c, b0, nb, c->n_ready)) return st;
+    if (c->find_unused) {
+      if (!c->dry_run) {
+        if (ddp_status_t st = finish_unused(c)) return st;
+      } else {
+        std::fill(c->used_local.begin(), c->used_local.end(), 0);
+      }
+    }
     if (!c->dry_run) {
       CUDA_TRY(c, cudaEventRecord(c->comm_done, c->comm));
       if (c->ce_used) {  // copy-engine reductions write .grad on the reduce stream
@@ -825,6 +941,9 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       if (v < DDP_ALGO_AUTO || v > DDP_ALGO_CE) return fail(DDP_ERR_INVALID_ARG, "bad algo");
       c->algo = v;
       break;
+    case DDP_OPT_FIND_UNUSED:
+      c->find_unused = v ? 1 : 0;
+      break;
     case DDP_OPT_COMM_CTAS:
       if (v < 1 || v > 148) return fail(DDP_ERR_INVALID_ARG, "COMM_CTAS must be in [1, 148]");
       c->comm_ctas = v;
@@ -859,6 +978,7 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_ALGO: *v = c->algo; break;
     case DDP_OPT_PACK_CTAS: *v = c->pack_ctas; break;
     case DDP_OPT_P2P_STAGE_BYTES: *v = c->stage_bytes; break;
+    case DDP_OPT_FIND_UNUSED: *v = c->find_unused; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;

@@ -65,6 +65,17 @@ cudaError_t launch_p2p(int algo, int dtype, const SlotView& sv, const P2PLaunch&
 // slot q of element x at slot0 + q * stride_elems + x.
 cudaError_t launch_ce_reduce(int dtype, int world, const SlotView& sv, const void* slot0, int64_t stride_elems,
                              int max_ctas, cudaStream_t s);
+// Locally-unused parameters (find_unused): copy src (library scratch holding the
+// average) -> dst (the caller's gradient) where global_used[param] > 0.
+struct UnusedView {
+  const void* const* src;
+  void* const* dst;
+  const int32_t* param;
+  const int64_t* numel;
+  int32_t n;
+};
+cudaError_t launch_unused_fixup(int dtype, const UnusedView& uv, const int32_t* global_used, int max_ctas,
+                                cudaStream_t s);
 // Largest number of CTAs per rank an emulated launch of `world` ranks may use.
 int emulated_max_ctas(int algo, int dtype, int n_slots, int world);
 

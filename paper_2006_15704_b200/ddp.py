@@ -13,6 +13,7 @@ P:L186 / L306).  Every step of the synchronization runs in
 from __future__ import annotations
 
 import contextlib
+import dataclasses
 from typing import Dict, Iterable, List, Optional, Sequence
 
 import torch
@@ -106,6 +107,14 @@ class GradReducer:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         L.ddp_grads_ready(self.ctx, batch, s.cuda_stream)
 
+    def mark_unused(self, param_idx: int, grad: Optional[torch.Tensor],
+                    stream: Optional[torch.cuda.Stream] = None):
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        L.ddp_mark_unused(self.ctx, param_idx, 0 if grad is None else grad.data_ptr(), s.cuda_stream)
+
+    def global_unused(self) -> List[bool]:
+        return L.ddp_global_unused(self.ctx, len(self.numels))
+
     def finalize(self, stream: Optional[torch.cuda.Stream] = None):
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         L.ddp_finalize_backward(self.ctx, s.cuda_stream)
@@ -139,6 +148,22 @@ class GradReducer:
             pass
 
 
+def _tensors(x):
+    """Every tensor inside a (nested) forward output: tensors, sequences,
+    mappings and dataclass-like objects (e.g. HF ModelOutput)."""
+    if isinstance(x, torch.Tensor):
+        yield x
+    elif isinstance(x, dict):
+        for v in x.values():
+            yield from _tensors(v)
+    elif isinstance(x, (list, tuple)):
+        for v in x:
+            yield from _tensors(v)
+    elif dataclasses.is_dataclass(x) and not isinstance(x, type):
+        for f in dataclasses.fields(x):
+            yield from _tensors(getattr(x, f.name))
+
+
 class DistributedDataParallel(torch.nn.Module):
     """Wraps a module; gradients of its parameters are bucketed, averaged across
     the process group and written back into ``.grad`` during backward.
@@ -150,8 +175,13 @@ class DistributedDataParallel(torch.nn.Module):
     """
 
     def __init__(self, module: torch.nn.Module, process_group=None, bucket_cap_mb: float = 25,
-                 broadcast_parameters: bool = True, options: Optional[Dict[int, int]] = None):
+                 broadcast_parameters: bool = True, options: Optional[Dict[int, int]] = None,
+                 find_unused_parameters: bool = False):
         super().__init__()
+        self.find_unused_parameters = find_unused_parameters
+        options = dict(options or {})
+        if find_unused_parameters:
+            options[L.OPT_FIND_UNUSED] = 1
         self.module = module
         self.params = [p for p in module.parameters() if p.requires_grad]
         dtypes = {p.dtype for p in self.params}
@@ -165,6 +195,9 @@ class DistributedDataParallel(torch.nn.Module):
                                    int(bucket_cap_mb * MIB), group=process_group,
                                    device=self.params[0].device, options=options)
         self._pass_open = False
+        self._in_no_sync = False
+        self._unused_bufs: Dict[int, torch.Tensor] = {}
+        self._param_index = {id(p): i for i, p in enumerate(self.params)}
         self._hooks = [p.register_post_accumulate_grad_hook(self._make_hook(i))
                        for i, p in enumerate(self.params)]
 
@@ -183,9 +216,66 @@ class DistributedDataParallel(torch.nn.Module):
     def _finalize(self):
         self._pass_open = False
         self.reducer.finalize()
+        if self._unused_bufs:
+            # locally-unused params without a .grad got a zero buffer as their
+            # destination; attach it only where some rank used the param (the
+            # bitmap read blocks on the extra allreduce, as P:L310 implies)
+            gu = self.reducer.global_unused()
+            for i, buf in self._unused_bufs.items():
+                if not gu[i]:
+                    self.params[i].grad = buf
+            self._unused_bufs = {}
 
     def forward(self, *args, **kwargs):
-        return self.module(*args, **kwargs)
+        out = self.module(*args, **kwargs)
+        if self.find_unused_parameters and torch.is_grad_enabled():
+            self._mark_unused(out)
+        return out
 
+    def _mark_unused(self, out):
+        """Alg. 1 forward (L224-L225): traverse the autograd graph from the
+        outputs; parameters not reached get no gradient this pass and are
+        marked ready now."""
+        used = set()
+        stack, seen = [], set()
+        for t in _tensors(out):
+            if t.requires_grad:
+                if t.grad_fn is not None:
+                    stack.append(t.grad_fn)
+                elif id(t) in self._param_index:
+                    used.add(id(t))
+        while stack:
+            fn = stack.pop()
+            if fn in seen:
+                continue
+            seen.add(fn)
+            var = getattr(fn, "variable", None)
+            if var is not None:
+                used.add(id(var))
+            for nxt, _ in fn.next_functions:
+                if nxt is not None:
+                    stack.append(nxt)
+        for i, p in enumerate(self.params):
+            if id(p) in used:
+                continue
+            g = p.grad
+            if g is None and not self._in_no_sync:
+                g = self._unused_bufs[i] = torch.zeros_like(p)
+            self.reducer.mark_unused(i, g)
+
+    @contextlib.contextmanager
     def no_sync(self):
-        return self.reducer.no_sync()
+        with self.reducer.no_sync():
+            self._in_no_sync = True
+            try:
+                yield
+            finally:
+                self._in_no_sync = False
+
+    def close(self):
+        """Removes the hooks and releases the native context (the module can be
+        wrapped again, e.g. with another bucket cap)."""
+        for h in self._hooks:
+            h.remove()
+        self._hooks = []
+        self.reducer.close()

@@ -238,3 +238,64 @@ def test_algorithm_selection_and_storage_layout():
         assert {L.ddp_bucket_algo(one, b) for b in range(L.ddp_num_buckets(one))} == {L.ALGO_ONESHOT}
     finally:
         L.ddp_destroy(one)
+
+
+def test_mark_unused_protocol():
+    """ddp_mark_unused is a ready signal (Alg. 1 forward L224-L225): buckets
+    holding unused params launch without their hooks, in order (O-2 replay of
+    the combined signal sequence); it needs FIND_UNUSED; duplicates are errors;
+    FIND_UNUSED adds the bitmap + scratch to the storage."""
+    ns = numels("toy")
+    ctx = L.ddp_create(ns, L.FP32, 4096, 2, 0)
+    try:
+        base = L.ddp_storage_bytes(ctx)
+        L.ddp_set_option(ctx, L.OPT_DRY_RUN, 1)
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_mark_unused(ctx, 0, 0, 0)
+        assert e.value.status == L.ERR_STATE
+        L.ddp_set_option(ctx, L.OPT_FIND_UNUSED, 1)
+        assert L.ddp_storage_bytes(ctx) >= base + sum(ns) * 4 + len(ns) * 4
+        a = assign_buckets(ns, 4, 4096)
+        rng = random.Random(7)
+        for _ in range(20):
+            unused = [p for p in range(len(ns)) if rng.random() < 0.4]
+            order = unused + [p for p in range(len(ns) - 1, -1, -1) if p not in unused]
+            for p in order:
+                if p in unused:
+                    L.ddp_mark_unused(ctx, p, 0, 0)
+                else:
+                    L.ddp_grad_ready(ctx, p, 0, 0)
+            L.ddp_finalize_backward(ctx, 0)
+            assert L.ddp_launch_trace(ctx) == replay(a, order)
+        L.ddp_mark_unused(ctx, 2, 0, 0)
+        for bad in (lambda: L.ddp_mark_unused(ctx, 2, 0, 0), lambda: L.ddp_grad_ready(ctx, 2, 0, 0)):
+            with pytest.raises(L.DDPError) as e:
+                bad()
+            assert e.value.status == L.ERR_DUPLICATE
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_global_unused(ctx, len(ns))
+        assert e.value.status == L.ERR_STATE      # dry run: no bitmap allreduce ever ran
+    finally:
+        L.ddp_destroy(ctx)
+
+
+def test_mark_unused_accumulated_grad_required():
+    """A param that got a gradient in a no_sync pass participates in the next
+    synced pass: marking it unused then needs its accumulated grad."""
+    ns = numels("toy")
+    ctx = L.ddp_create(ns, L.FP32, 4096, 2, 0)
+    try:
+        L.ddp_set_option(ctx, L.OPT_DRY_RUN, 1)
+        L.ddp_set_option(ctx, L.OPT_FIND_UNUSED, 1)
+        L.ddp_no_sync_begin(ctx)
+        for p in range(len(ns)):
+            L.ddp_grad_ready(ctx, p, 0, 0)
+        L.ddp_finalize_backward(ctx, 0)
+        L.ddp_no_sync_end(ctx)
+        L.ddp_set_option(ctx, L.OPT_DRY_RUN, 1)
+        L.ddp_mark_unused(ctx, 0, 0, 0)   # dry run: pointers are not checked
+        for p in range(1, len(ns)):
+            L.ddp_grad_ready(ctx, p, 0, 0)
+        L.ddp_finalize_backward(ctx, 0)
+    finally:
+        L.ddp_destroy(ctx)
