@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--comm-ctas", type=int, default=0)
     ap.add_argument("--pack-ctas", type=int, default=0)
     ap.add_argument("--stage-kib", type=int, default=0)
+    ap.add_argument("--ce-streams", type=int, default=0)
     ap.add_argument("--exposed-model", default="resnet50", choices=["none", "resnet50", "bert_large"],
                     help="real-model backward for the exposed-time measurement")
     ap.add_argument("--exposed-batch", type=int, default=0)
@@ -215,6 +216,8 @@ def run_ours(a):
         opts[L.OPT_PACK_CTAS] = a.pack_ctas
     if a.stage_kib:
         opts[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
+    if a.ce_streams:
+        opts[L.OPT_CE_STREAMS] = a.ce_streams
     if a.oneshot_max >= 0:
         opts[L.OPT_P2P_ONESHOT_MAX] = a.oneshot_max
     if a.twoshot_max >= 0:
@@ -289,41 +292,57 @@ def run_ours(a):
     bnumel = red.bucket_numels()
     S_tot = sum(bnumel) * esize
     # our kernel launches per step (NCCL's own kernels excluded)
-    launches_per_step = sum(prof[k][1] for k in ("pack", "unpack", "p2p_fused")) / kprof_steps
+    launches_per_step = sum(prof[k][1] for k in ("pack", "unpack", "p2p_fused", "ce_reduce")) / kprof_steps
 
     # dominant kernel roofline: algorithmic bytes per launch / measured launch time
     peak_hbm, peak_src = measured_peaks()
     kinds = {k: v for k, v in prof.items() if v[1] > 0}
     dom = max(kinds, key=lambda k: kinds[k][0]) if kinds else None
+    small = 0   # CE buckets: bytes of the gradients gathered by the pack kernel (< 1 MiB each)
+    for b, x in enumerate(algos):
+        if x == "ce":
+            for s_ in range(L.ddp_bucket_info(red.ctx, b)[1]):
+                p, _ = L.ddp_bucket_slot(red.ctx, b, s_)
+                small += ns[p] * esize if ns[p] * esize < (1 << 20) else 0
+    by = {x: sum(n * esize for n, y in zip(bnumel, algos) if y == x) for x in ("nccl", "oneshot", "twoshot", "ce", "nvls")}
+
+    def kind_bytes(kind):
+        """(algorithmic bytes per step, bound, rule) of one profile kind."""
+        if kind == "p2p_fused" and world == 1:
+            return 3 * (by["oneshot"] + by["twoshot"]), "hbm", "3 x bucket bytes (read g, write bucket, write g)"
+        if kind == "pack":
+            return 2 * (by["nccl"] + small), "hbm", "2 x bytes packed (NCCL buckets; CE small gradients)"
+        if kind == "unpack":
+            return 2 * by["nccl"], "hbm", "2 x bucket bytes"
+        if kind == "p2p_fused":
+            return (by["oneshot"] * (world - 1) + by["twoshot"] * 2 * (world - 1) / world
+                    + by["nvls"] * (1 + 1 / world), "nvlink",
+                    "NVLink bytes per direction: one-shot (W-1)S, two-shot 2(W-1)/W S, NVLS (1+1/W)S")
+        if kind == "ce_copy":
+            return by["ce"] * (world - 1), "nvlink", "copy-engine NVLink bytes per direction (W-1)S"
+        if kind == "ce_reduce":
+            return by["ce"] * (world + 1), "hbm", "(W+1) x bucket bytes (W operands read, .grad written)"
+        return 2 * (world - 1) / world * by["nccl"], "nvlink", "ring 2(W-1)/W x bucket bytes"
+
+    def roof_of(kind):
+        tot_ms, cnt = kinds[kind]
+        avg_ms = tot_ms / cnt
+        step_bytes, bound, per = kind_bytes(kind)
+        byts = step_bytes / (cnt / kprof_steps)
+        peak = peak_hbm if bound == "hbm" else 770.0
+        r_ = {"bound": bound, "achieved": byts / (avg_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s"}
+        r_["frac"] = r_["achieved"] / peak
+        r_["traffic"], r_["traffic_source"] = ncu_traffic(workload_name(a), world, kind)
+        r_.update(kernel=kind, algorithmic_bytes_per_launch=byts, bytes_rule=per, avg_launch_ms=avg_ms,
+                  peak_source=(f"MEASURED_PEAKS.json hbm_gbs ({peak_src})" if bound == "hbm"
+                               else "B200_PROFILING.md measured peer copy 770 GB/s per direction"))
+        return r_
     roof = None
     if dom is not None:
-        tot_ms, cnt = kinds[dom]
-        avg_ms = tot_ms / cnt
-        per_step_launches = cnt / kprof_steps
-        p2p = [(n * esize, x) for n, x in zip(bnumel, algos) if x != "nccl"]
-        ncl = [n * esize for n, x in zip(bnumel, algos) if x == "nccl"]
-        if dom == "p2p_fused" and world == 1:
-            # world 1 fused kernel: read grad S, write bucket S, write grad S (3 S per bucket)
-            step_bytes, bound, per = 3 * sum(b for b, _ in p2p), "hbm", "3 x bucket bytes"
-        elif dom in ("pack", "unpack"):
-            step_bytes, bound, per = 2 * sum(ncl), "hbm", "2 x bucket bytes"
-        elif dom == "p2p_fused":
-            # NVLink bytes sent per GPU per direction: one-shot (W-1) S, two-shot 2 (W-1)/W S
-            step_bytes = sum(b * ((world - 1) if x == "oneshot" else 2 * (world - 1) / world) for b, x in p2p)
-            bound, per = "nvlink", "NVLink bytes per direction: one-shot (W-1)S, two-shot 2(W-1)/W S"
-        else:
-            step_bytes, bound, per = 2 * (world - 1) / world * sum(ncl), "nvlink", "2(W-1)/W x bucket bytes"
-        byts = step_bytes / per_step_launches
-        peak = peak_hbm if bound == "hbm" else 770.0
-        roof = {"bound": bound, "achieved": byts / (avg_ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s"}
-        roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"], roof["traffic_source"] = ncu_traffic(workload_name(a), world, dom)
-        roof["kernel"] = dom
-        roof["algorithmic_bytes_per_launch"] = byts
-        roof["bytes_rule"] = per
-        roof["peak_source"] = (f"MEASURED_PEAKS.json hbm_gbs ({peak_src})" if bound == "hbm"
-                               else "B200_PROFILING.md measured peer copy 770 GB/s per direction")
-        roof["avg_launch_ms"] = avg_ms
+        roof = roof_of(dom)
+        roof["all_kinds"] = {k: {"achieved": round(x["achieved"], 1), "frac": round(x["frac"], 3),
+                                 "bound": x["bound"], "ms_per_step": kinds[k][0] / kprof_steps}
+                             for k in kinds for x in [roof_of(k)]}
 
     # ---- bucket allreduce bus bandwidth on a 25 MiB bucket (N > 1) ------------------
     busbw = None
@@ -598,6 +617,8 @@ def _opts(a):
             o[key] = v
     if a.stage_kib:
         o[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
+    if a.ce_streams:
+        o[L.OPT_CE_STREAMS] = a.ce_streams
     if a.oneshot_max >= 0:
         o[L.OPT_P2P_ONESHOT_MAX] = a.oneshot_max
     if a.twoshot_max >= 0:
@@ -648,7 +669,7 @@ def allreduce_sweep(a, rank, world, local, dev, opts):
     tdt = torch.float32 if a.dtype == "fp32" else torch.bfloat16
     esize = 4 if a.dtype == "fp32" else 2
     stream = torch.cuda.current_stream(dev)
-    algos = [L.ALGO_AUTO, L.ALGO_NCCL, L.ALGO_ONESHOT, L.ALGO_TWOSHOT] + ([L.ALGO_CE] if world > 1 else [])
+    algos = [L.ALGO_AUTO, L.ALGO_NCCL, L.ALGO_ONESHOT, L.ALGO_TWOSHOT] + ([L.ALGO_CE, L.ALGO_NVLS] if world > 1 else [])
     sizes = [4 << 10, 64 << 10, 256 << 10, 1 << 20, 4 << 20, 16 << 20, 25 << 20, 64 << 20, 256 << 20]
     res = []
 

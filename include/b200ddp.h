@@ -74,14 +74,19 @@ enum {
   DDP_OPT_DRY_RUN = 5,          /* 1: protocol only, no device work (host tests; CREATED only) */
   DDP_OPT_PROFILE = 6,          /* 1: time every device launch with CUDA events */
   DDP_OPT_ALGO = 7,             /* force the bucket allreduce: 0 auto, 1 NCCL, 2 one-shot, 3 two-shot,
-                                   4 copy-engine one-shot (world > 1) */
+                                   4 copy-engine one-shot (world > 1), 5 NVLS (needs MULTICAST) */
   DDP_OPT_PACK_CTAS = 8,        /* max CTAs of pack/unpack kernels and of P2P kernels at world 1 */
   DDP_OPT_P2P_STAGE_BYTES = 9,  /* 0 (default): one pipeline stage per CTA chunk; else split each
                                    CTA chunk into stages of this many bytes (one sync per stage) */
-  DDP_OPT_FIND_UNUSED = 10      /* 1: globally-unused-parameter detection:
+  DDP_OPT_FIND_UNUSED = 10,     /* 1: globally-unused-parameter detection:
                                    enables ddp_mark_unused, a participation bitmap and one extra
                                    allreduce per synced pass; CREATED only (storage grows by one
                                    bucket-region-sized scratch + the bitmap) */
+  DDP_OPT_MULTICAST = 11,       /* 1: the caller will pass a multicast (NVLS) address of the storage
+                                   to ddp_bind_device, enabling DDP_ALGO_NVLS; CREATED only.  Every
+                                   rank must agree.  Never increases ddp_storage_bytes */
+  DDP_OPT_CE_STREAMS = 12       /* copy-engine algorithm: number of streams its peer copies are
+                                   spread over (1..16, default 4); before binding only */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.
@@ -90,8 +95,12 @@ enum {
  *   TWOSHOT: one fused sm_100a kernel: pack + reduce-scatter push, reduce, all-gather push, unpack
  *   CE:      pack kernel -> copy-engine pushes (cudaMemcpyAsync over NVLink) ordered by stream
  *            memory operations (no SM waits) -> rank-order reduce kernel into .grad on a second
- *            stream.  Frees the SMs for the overlapped backward. */
-enum { DDP_ALGO_AUTO = 0, DDP_ALGO_NCCL = 1, DDP_ALGO_ONESHOT = 2, DDP_ALGO_TWOSHOT = 3, DDP_ALGO_CE = 4 };
+ *            stream.  Frees the SMs for the overlapped backward.
+ *   NVLS:    one fused sm_100a kernel: pack -> multimem.ld_reduce / multimem.st through the
+ *            NVSwitch multicast address ((1+1/W) S NVLink bytes per direction) -> unpack.
+ *            Needs DDP_OPT_MULTICAST; otherwise resolves to TWOSHOT. */
+enum { DDP_ALGO_AUTO = 0, DDP_ALGO_NCCL = 1, DDP_ALGO_ONESHOT = 2, DDP_ALGO_TWOSHOT = 3, DDP_ALGO_CE = 4,
+       DDP_ALGO_NVLS = 5 };
 
 /* ---- construction (host only, deterministic, touches no GPU) -------------
  * Bucket assignment (Alg. 1 "allocate parameters to buckets in the
@@ -129,7 +138,9 @@ ddp_status_t ddp_bucket_algo(const ddp_ctx_t* ctx, int32_t b, int32_t* algo);
  *   peer_storage[world]: device addresses, valid on `device`, of every rank's
  *   storage (ddp_storage_bytes each, 256-B aligned, peer-mapped, e.g. torch
  *   symmetric memory); peer_storage[rank] is this rank's own.
- *   multicast_ptr: reserved (NVLS), may be NULL.
+ *   multicast_ptr: multicast (NVLS) address of this rank's storage base, i.e. the
+ *   address whose loads/stores reach the same offset of every rank's storage;
+ *   required iff DDP_OPT_MULTICAST is set, else ignored (may be NULL).
  * Errors: DDP_ERR_STATE (already bound), DDP_ERR_INVALID_ARG, DDP_ERR_CUDA,
  * DDP_ERR_NCCL. */
 ddp_status_t ddp_get_nccl_id(uint8_t out[128]);

@@ -23,9 +23,10 @@ STATUS_NAMES = ["OK", "INVALID_ARG", "STATE", "DUPLICATE", "INCOMPLETE", "CUDA",
                 "POISONED", "TIMEOUT", "UNSUPPORTED"]
 FP32, BF16 = 0, 1
 OPT_OVERLAP, OPT_P2P_ONESHOT_MAX, OPT_P2P_TWOSHOT_MAX, OPT_COMM_CTAS, OPT_DRY_RUN, OPT_PROFILE, \
-    OPT_ALGO, OPT_PACK_CTAS, OPT_P2P_STAGE_BYTES, OPT_FIND_UNUSED = range(1, 11)
-ALGO_AUTO, ALGO_NCCL, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_CE = range(5)
-ALGO_NAMES = {ALGO_NCCL: "nccl", ALGO_ONESHOT: "oneshot", ALGO_TWOSHOT: "twoshot", ALGO_CE: "ce"}
+    OPT_ALGO, OPT_PACK_CTAS, OPT_P2P_STAGE_BYTES, OPT_FIND_UNUSED, OPT_MULTICAST, OPT_CE_STREAMS = range(1, 13)
+ALGO_AUTO, ALGO_NCCL, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_CE, ALGO_NVLS = range(6)
+ALGO_NAMES = {ALGO_NCCL: "nccl", ALGO_ONESHOT: "oneshot", ALGO_TWOSHOT: "twoshot", ALGO_CE: "ce",
+              ALGO_NVLS: "nvls"}
 PROFILE_KINDS = ("pack", "nccl_allreduce", "unpack", "p2p_fused", "ce_copy", "ce_reduce")
 
 

@@ -45,6 +45,11 @@ constexpr int64_t kMinChunkElems = 4096;   // smallest per-CTA chunk worth a CTA
 // stage per chunk (one sync for one-shot, two for two-shot); DDP_OPT_P2P_STAGE_BYTES
 // splits chunks for experiments.
 constexpr int64_t kBarrierScratch = 32 * 1024;  // scratch int inside the flags region
+// Copy-engine algorithm: gradients of at least this many bytes travel straight
+// from .grad (one cudaMemcpyAsync per peer); smaller ones are gathered into one
+// region first (a copy-engine transfer costs a few us of fixed latency).
+constexpr int64_t kCeDirectBytes = 1 << 20;
+constexpr int64_t kCeWireAlign = 64;  // elements: wire offsets keep 16-B (and 256-B) alignment
 
 struct Bucket {
   int64_t numel = 0;
@@ -56,8 +61,11 @@ struct Bucket {
   int ctas = 1;
   int64_t shard = 0, chunk = 0, sub = 0;
   int32_t stages = 0;
-  // copy-engine algorithm: W slots at ce_off + q * ce_stride; passes launched so far
-  int64_t ce_off = 0, ce_stride = 0;
+  // copy-engine algorithm: W slots at ce_off + q * ce_stride (wire layout: direct
+  // gradients, then the gathered small ones from ce_small0); passes launched so far
+  int64_t ce_off = 0, ce_stride = 0, ce_small0 = 0, ce_wire_numel = 0;
+  std::vector<int64_t> ce_wire;     // per slot: element offset in a slot
+  std::vector<uint8_t> ce_direct;   // per slot: copied by the copy engine straight from .grad
   uint32_t ce_count = 0;
 };
 
@@ -84,7 +92,7 @@ struct ddp_ctx {
   // NVLink bytes as two-shot with one sync instead of two; world > 2: <= 512 KiB)
   int64_t overlap = 1, oneshot_max = -1, twoshot_max = INT64_MAX, comm_ctas = 64,
           dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 8, stage_bytes = 0,
-          find_unused = 0;
+          find_unused = 0, multicast = 0, ce_streams = 4;
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
           stage1_stride = 0, ce_flags_off = 0, bitmap_off = 0, scratch_off = 0, storage_bytes = 0;
@@ -101,7 +109,13 @@ struct ddp_ctx {
   bool bitmap_valid = false;
   // copy-engine path: reduce stream, events, driver stream-memory-op entry points
   cudaStream_t ce_red = nullptr, ce_pack = nullptr;
-  std::vector<cudaEvent_t> ce_packed;  // per bucket: own slot packed (comm -> reduce stream)
+  std::vector<cudaStream_t> ce_cp;          // copy streams: copies of one bucket spread over them
+  std::vector<cudaEvent_t> ce_go;           // per bucket: copies may start (comm -> copy streams)
+  std::vector<cudaEvent_t> ce_cp_done;      // per bucket x copy stream: its copies issued
+  std::vector<cudaEvent_t> ce_packed;  // per bucket: small gradients gathered (pack -> comm stream)
+  std::vector<cudaEvent_t> ce_copied;  // per bucket: copies issued (comm -> reduce stream)
+  std::vector<void*> ce_grad;          // scratch argument arrays
+  std::vector<int64_t> ce_wire, ce_numel;
   cudaEvent_t ce_red_done = nullptr;
   void* fn_write32 = nullptr;
   void* fn_wait32 = nullptr;
@@ -119,6 +133,7 @@ struct ddp_ctx {
   cudaStream_t comm = nullptr;
   ncclComm_t nccl = nullptr;
   void* storage[kMaxWorld] = {};
+  void* mc = nullptr;  // NVLS multicast address of the storage base
   int64_t grad_rank_stride = 0;
   std::vector<cudaStream_t> unwaited;  // producer streams since the last event wait
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> stream_events;
@@ -192,13 +207,21 @@ void assign(ddp_ctx* c) {
 int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   const int64_t bytes = bk.numel * c->esize;
   int a;
-  if (c->algo != DDP_ALGO_AUTO) a = (c->algo == DDP_ALGO_CE && c->world == 1) ? DDP_ALGO_ONESHOT : (int)c->algo;
-  else if (c->world == 1) a = DDP_ALGO_ONESHOT;
-  else if (bytes <= (c->oneshot_max >= 0 ? c->oneshot_max : c->world == 2 ? INT64_MAX : 512 * 1024))
+  if (c->algo != DDP_ALGO_AUTO) {
+    a = (int)c->algo;
+    if (c->world == 1 && (a == DDP_ALGO_CE || a == DDP_ALGO_NVLS)) a = DDP_ALGO_ONESHOT;
+    if (a == DDP_ALGO_NVLS && !c->multicast) a = DDP_ALGO_TWOSHOT;
+  } else if (c->world == 1) {
     a = DDP_ALGO_ONESHOT;
-  else if (bytes <= c->twoshot_max) a = DDP_ALGO_TWOSHOT;
-  else a = DDP_ALGO_NCCL;
-  if ((a == DDP_ALGO_ONESHOT || a == DDP_ALGO_TWOSHOT) && (int)bk.params.size() > kMaxSlotsPerLaunch)
+  } else if (bytes <= (c->oneshot_max >= 0 ? c->oneshot_max : c->world == 2 ? INT64_MAX : 512 * 1024)) {
+    a = DDP_ALGO_ONESHOT;
+  } else if (bytes <= c->twoshot_max) {
+    a = c->multicast ? DDP_ALGO_NVLS : DDP_ALGO_TWOSHOT;
+  } else {
+    a = DDP_ALGO_NCCL;
+  }
+  if ((a == DDP_ALGO_ONESHOT || a == DDP_ALGO_TWOSHOT || a == DDP_ALGO_CE || a == DDP_ALGO_NVLS) &&
+      (int)bk.params.size() > kMaxSlotsPerLaunch)
     a = DDP_ALGO_NCCL;
   return a;
 }
@@ -210,8 +233,8 @@ void grid_for(const ddp_ctx* c, Bucket& bk, int max_ctas) {
     bk.shard = bk.chunk = 0;
     return;
   }
-  const int64_t L = bk.algo == DDP_ALGO_TWOSHOT ? align_up(cdiv(bk.numel, c->world), kAlignElems)
-                                                 : align_up(bk.numel, kAlignElems);
+  const bool sharded = bk.algo == DDP_ALGO_TWOSHOT || bk.algo == DDP_ALGO_NVLS;
+  const int64_t L = sharded ? align_up(cdiv(bk.numel, c->world), kAlignElems) : align_up(bk.numel, kAlignElems);
   int64_t C = std::min<int64_t>(max_ctas, std::max<int64_t>(1, cdiv(L, kMinChunkElems)));
   const int64_t Q = align_up(cdiv(L, C), kAlignElems);
   C = std::max<int64_t>(1, cdiv(L, Q));
@@ -254,8 +277,26 @@ void plan(ddp_ctx* c) {
   pos += align_up((int64_t)c->buckets.size() * kMaxWorld * 2 * 4, 256);
   for (Bucket& bk : c->buckets) {
     bk.ce_stride = 0;
+    bk.ce_wire.clear();
+    bk.ce_direct.clear();
     if (bk.algo != DDP_ALGO_CE) continue;
-    bk.ce_stride = align_up(bk.numel * c->esize, 256);
+    const size_t ns = bk.params.size();
+    bk.ce_wire.assign(ns, 0);
+    bk.ce_direct.assign(ns, 0);
+    int64_t w = 0;
+    for (int pass = 0; pass < 2; ++pass) {  // direct gradients first, then the small ones
+      if (pass == 1) bk.ce_small0 = w;
+      for (size_t k = 0; k < ns; ++k) {
+        const int64_t n = bk.off[k + 1] - bk.off[k];
+        const bool direct = n * c->esize >= kCeDirectBytes;
+        if (direct != (pass == 0)) continue;
+        bk.ce_direct[k] = direct;
+        bk.ce_wire[k] = w;
+        w = align_up(w + n, kCeWireAlign);
+      }
+    }
+    bk.ce_wire_numel = w;
+    bk.ce_stride = align_up(w * c->esize, 256);
     bk.ce_off = pos;
     pos += c->world * bk.ce_stride;
   }
@@ -325,45 +366,98 @@ ddp_status_t ce_wait(ddp_ctx* c, cudaStream_t s, uint32_t* addr, uint32_t v) {
   return DDP_OK;
 }
 
-// Copy-engine one-shot (SM-free exchange): pack own slot (kernel) -> copy-engine
-// push of the slot into every peer (cudaMemcpyAsync over NVLink) -> flag writes;
-// on the reduce stream: wait for every peer's flag -> rank-order reduction of
-// the W slots straight into .grad (kernel) -> "consumed" flags, which guard the
-// next pass's pushes into this bucket's slots.  No SM spins while waiting.
-ddp_status_t launch_ce(ddp_ctx* c, int b, const SlotView& sv, float scale) {
+// Copy-engine one-shot (SM-free exchange).  Rank r's raw gradients go to slot r
+// of every peer: large ones by one cudaMemcpyAsync each straight from .grad,
+// the small ones gathered (kernel) into r's own slot and sent as one region.
+// Stream memory operations order everything, so no SM spins while waiting:
+//   comm stream:    [wait: peers consumed pass v-1] -> copies -> ready flags to peers
+//   reduce stream:  [wait: own copies issued, peers' ready flags] -> rank-order
+//                   reduce x 1/W per operand straight into .grad -> consumed flags
+ddp_status_t launch_ce(ddp_ctx* c, int b) {
   Bucket& bk = c->buckets[b];
   const int W = c->world, r = c->rank;
   char* mine = static_cast<char*>(c->storage[r]);
+  char* own_slot = mine + bk.ce_off + r * bk.ce_stride;
   const uint32_t v = ++bk.ce_count;
-  const int64_t bytes = bk.numel * c->esize;
-  // pack on its own stream so bucket b+1 packs while bucket b is on the copy engines
-  prof_begin(c, 0, c->ce_pack);
-  CUDA_TRY(c, launch_pack(c->dtype, sv, mine + bk.ce_off + r * bk.ce_stride, scale, (int)c->pack_ctas,
-                          c->ce_pack));
-  prof_end(c, c->ce_pack);
-  CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
-  CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_packed[b], 0));
+  const size_t ns = bk.params.size();
+  c->ce_grad.clear();
+  c->ce_wire.clear();
+  c->ce_numel.clear();
+  for (size_t k = 0; k < ns; ++k) {
+    if (bk.ce_direct[k]) continue;
+    c->ce_grad.push_back(bk.grads[k]);
+    c->ce_wire.push_back(bk.ce_wire[k]);
+    c->ce_numel.push_back(bk.off[k + 1] - bk.off[k]);
+  }
+  const bool any_small = !c->ce_grad.empty();
+  if (any_small) {  // gather on its own stream so it overlaps the previous bucket's copies
+    const CeView gv{c->ce_grad.data(), c->ce_wire.data(), c->ce_numel.data(), (int32_t)c->ce_grad.size()};
+    prof_begin(c, 0, c->ce_pack);
+    CUDA_TRY(c, launch_ce_gather(c->dtype, gv, own_slot, (int)c->pack_ctas, c->ce_pack));
+    prof_end(c, c->ce_pack);
+    CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_packed[b], 0));
+  }
   // reuse guard: every peer has consumed (reduced) its slot r of this bucket from pass v-1
   if (v > 1)
     for (int i = 1; i < W; ++i)
       if (ddp_status_t st = ce_wait(c, c->comm, ce_flag(c, r, 1, b, (r + i) % W), v - 1)) return st;
+  // Copies spread over the copy streams (each transfer carries a few us of fixed
+  // latency; independent streams let several copy engines overlap it), the
+  // largest-first into the least loaded stream.
+  const int K = (int)c->ce_cp.size();
   prof_begin(c, 4);
+  CUDA_TRY(c, cudaEventRecord(c->ce_go[b], c->comm));
+  int64_t load[16] = {};
+  bool used[16] = {};
+  auto issue = [&](void* dst, const void* src, int64_t bytes) -> ddp_status_t {
+    int best = 0;
+    for (int q = 1; q < K; ++q)
+      if (load[q] < load[best]) best = q;
+    if (!used[best]) {
+      CUDA_TRY(c, cudaStreamWaitEvent(c->ce_cp[best], c->ce_go[b], 0));
+      used[best] = true;
+    }
+    load[best] += bytes + (1 << 20);  // + fixed cost of a transfer, in bytes
+    CUDA_TRY(c, cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, c->ce_cp[best]));
+    return DDP_OK;
+  };
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
-    CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->storage[j]) + bk.ce_off + r * bk.ce_stride,
-                                mine + bk.ce_off + r * bk.ce_stride, bytes, cudaMemcpyDeviceToDevice, c->comm));
+    char* dst = static_cast<char*>(c->storage[j]) + bk.ce_off + r * bk.ce_stride;
+    for (size_t k = 0; k < ns; ++k)
+      if (bk.ce_direct[k])
+        if (ddp_status_t st = issue(dst + bk.ce_wire[k] * c->esize, bk.grads[k], (bk.off[k + 1] - bk.off[k]) * c->esize))
+          return st;
+    if (any_small)
+      if (ddp_status_t st = issue(dst + bk.ce_small0 * c->esize, own_slot + bk.ce_small0 * c->esize,
+                                  (bk.ce_wire_numel - bk.ce_small0) * c->esize))
+        return st;
+  }
+  for (int q = 0; q < K; ++q) {
+    if (!used[q]) continue;
+    cudaEvent_t e = c->ce_cp_done[(size_t)b * K + q];
+    CUDA_TRY(c, cudaEventRecord(e, c->ce_cp[q]));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->comm, e, 0));
   }
   prof_end(c);
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
     if (ddp_status_t st = ce_write(c, c->comm, ce_flag(c, j, 0, b, r), v)) return st;
   }
-  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_red, c->ce_packed[b], 0));
+  // the reduction overwrites .grad, which the copies above read: order after them
+  CUDA_TRY(c, cudaEventRecord(c->ce_copied[b], c->comm));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_red, c->ce_copied[b], 0));
   for (int i = 1; i < W; ++i)
     if (ddp_status_t st = ce_wait(c, c->ce_red, ce_flag(c, r, 0, b, (r + i) % W), v)) return st;
+  c->ce_grad.assign(bk.grads.begin(), bk.grads.end());
+  c->ce_wire.assign(bk.ce_wire.begin(), bk.ce_wire.end());
+  c->ce_numel.clear();
+  for (size_t k = 0; k < ns; ++k) c->ce_numel.push_back(bk.off[k + 1] - bk.off[k]);
+  const CeView rv{c->ce_grad.data(), c->ce_wire.data(), c->ce_numel.data(), (int32_t)ns};
   prof_begin(c, 5, c->ce_red);
-  CUDA_TRY(c, launch_ce_reduce(c->dtype, W, sv, mine + bk.ce_off, bk.ce_stride / c->esize, (int)c->pack_ctas,
-                               c->ce_red));
+  CUDA_TRY(c, launch_ce_reduce(c->dtype, W, r, rv, mine + bk.ce_off, bk.ce_stride, 1.0f / (float)W,
+                               (int)c->pack_ctas, c->ce_red));
   prof_end(c, c->ce_red);
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
@@ -379,7 +473,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   const SlotView sv{bk.off.data(), bk.grads.data(), (int32_t)bk.params.size()};
   const float scale = 1.0f / (float)c->world;  // fl(1/W), reading C-2
   char* mine = static_cast<char*>(c->storage[c->rank]);
-  if (bk.algo == DDP_ALGO_CE) return launch_ce(c, b, sv, scale);
+  if (bk.algo == DDP_ALGO_CE) return launch_ce(c, b);
   if (bk.algo == DDP_ALGO_NCCL) {
     void* buf = mine + bk.byte_off;
     prof_begin(c, 0);
@@ -421,10 +515,12 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   a.scale = scale;
   a.grad_rank_stride = c->grad_rank_stride;
   a.err = c->err_dev;
+  a.mc = c->mc;
   c->p2p_seq += (uint32_t)bk.stages + 2;  // flag values used: seq .. seq + stages + 1
   c->p2p_launches += 1;
   prof_begin(c, 3);
-  CUDA_TRY(c, launch_p2p(bk.algo, c->dtype, sv, a, c->comm));
+  if (bk.algo == DDP_ALGO_NVLS) CUDA_TRY(c, launch_nvls(c->dtype, sv, a, c->comm));
+  else CUDA_TRY(c, launch_p2p(bk.algo, c->dtype, sv, a, c->comm));
   prof_end(c);
   return DDP_OK;
 }
@@ -490,6 +586,7 @@ ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
     CUDA_TRY(c, cudaEventRecord(ev, s));
     CUDA_TRY(c, cudaStreamWaitEvent(c->comm, ev, 0));
     if (c->ce_pack) CUDA_TRY(c, cudaStreamWaitEvent(c->ce_pack, ev, 0));
+    for (cudaStream_t q : c->ce_cp) CUDA_TRY(c, cudaStreamWaitEvent(q, ev, 0));
   }
   c->unwaited.clear();
   if (c->world == 1 && !c->emulated) {
@@ -610,7 +707,7 @@ ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s, b
 
 bool is_layout_key(int32_t k) {
   return k == DDP_OPT_P2P_ONESHOT_MAX || k == DDP_OPT_P2P_TWOSHOT_MAX || k == DDP_OPT_ALGO ||
-         k == DDP_OPT_FIND_UNUSED;
+         k == DDP_OPT_FIND_UNUSED || k == DDP_OPT_MULTICAST;
 }
 
 }  // namespace
@@ -671,12 +768,18 @@ void ddp_destroy(ddp_ctx_t* c) {
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->prof_ready) cudaEventDestroy(e);
   if (c->comm_done) cudaEventDestroy(c->comm_done);
-  for (cudaStream_t s : {c->ce_red, c->ce_pack}) {
+  std::vector<cudaStream_t> own = c->ce_cp;
+  own.push_back(c->ce_red);
+  own.push_back(c->ce_pack);
+  for (cudaStream_t s : own) {
     if (!s) continue;
     if (!c->poisoned) cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
   }
+  for (cudaEvent_t e : c->ce_go) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ce_cp_done) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ce_packed) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ce_copied) cudaEventDestroy(e);
   if (c->ce_red_done) cudaEventDestroy(c->ce_red_done);
   if (c->err_host) cudaFreeHost(c->err_host);
   if (c->bitmap_host) cudaFreeHost(c->bitmap_host);
@@ -751,8 +854,10 @@ static ddp_status_t bind_common(ddp_ctx* c, int32_t device, void* comm_stream) {
 
 ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id[128], void* comm_stream,
                              void* const* peer_storage, void* multicast_ptr) {
-  (void)multicast_ptr;
   if (ddp_status_t st = check_ctx(c)) return st;
+  if (c->multicast && (!multicast_ptr || (reinterpret_cast<uintptr_t>(multicast_ptr) & 255)))
+    return fail(DDP_ERR_INVALID_ARG, "DDP_OPT_MULTICAST needs a 256-B aligned multicast address");
+  c->mc = c->multicast ? multicast_ptr : nullptr;
   if (c->bound || c->state != State::CREATED) return fail(DDP_ERR_STATE, "already bound");
   if (c->dry_run) return fail(DDP_ERR_STATE, "dry-run context cannot be bound");
   if (!nccl_id || !peer_storage) return fail(DDP_ERR_INVALID_ARG, "null argument");
@@ -777,6 +882,14 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_pack, cudaStreamNonBlocking, hi));
     c->ce_packed.assign(c->buckets.size(), nullptr);
     for (auto& e : c->ce_packed) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ce_copied.assign(c->buckets.size(), nullptr);
+    for (auto& e : c->ce_copied) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ce_cp.assign((size_t)c->ce_streams, nullptr);
+    for (auto& q : c->ce_cp) CUDA_TRY(c, cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
+    c->ce_go.assign(c->buckets.size(), nullptr);
+    for (auto& e : c->ce_go) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ce_cp_done.assign(c->buckets.size() * (size_t)c->ce_streams, nullptr);
+    for (auto& e : c->ce_cp_done) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->ce_red_done, cudaEventDisableTiming));
     cudaDriverEntryPointQueryResult q1, q2;
     CUDA_TRY(c, cudaGetDriverEntryPoint("cuStreamWriteValue32", &c->fn_write32, cudaEnableDefault, &q1));
@@ -807,6 +920,7 @@ ddp_status_t ddp_bind_emulated(ddp_ctx_t* c, int32_t device, void* comm_stream, 
     if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE)
       return fail(DDP_ERR_UNSUPPORTED, "emulation runs the one-shot / two-shot kernels only (set DDP_OPT_ALGO)");
   if (c->find_unused) return fail(DDP_ERR_UNSUPPORTED, "find_unused needs a real communicator (no emulation)");
+  if (c->multicast) return fail(DDP_ERR_UNSUPPORTED, "NVLS needs real multicast memory (no emulation)");
   if (ddp_status_t st = bind_common(c, device, comm_stream)) return st;
   for (int r = 0; r < c->world; ++r) c->storage[r] = storages[r];
   c->grad_rank_stride = grad_rank_stride_bytes;
@@ -938,12 +1052,20 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       c->twoshot_max = v;
       break;
     case DDP_OPT_ALGO:
-      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_CE) return fail(DDP_ERR_INVALID_ARG, "bad algo");
+      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_NVLS) return fail(DDP_ERR_INVALID_ARG, "bad algo");
       c->algo = v;
       break;
     case DDP_OPT_FIND_UNUSED:
       c->find_unused = v ? 1 : 0;
       break;
+    case DDP_OPT_MULTICAST:
+      c->multicast = v ? 1 : 0;
+      break;
+    case DDP_OPT_CE_STREAMS:
+      if (c->bound) return fail(DDP_ERR_STATE, "CE_STREAMS is fixed once bound");
+      if (v < 1 || v > 16) return fail(DDP_ERR_INVALID_ARG, "CE_STREAMS must be in [1, 16]");
+      c->ce_streams = v;
+      return DDP_OK;
     case DDP_OPT_COMM_CTAS:
       if (v < 1 || v > 148) return fail(DDP_ERR_INVALID_ARG, "COMM_CTAS must be in [1, 148]");
       c->comm_ctas = v;
@@ -979,6 +1101,8 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_PACK_CTAS: *v = c->pack_ctas; break;
     case DDP_OPT_P2P_STAGE_BYTES: *v = c->stage_bytes; break;
     case DDP_OPT_FIND_UNUSED: *v = c->find_unused; break;
+    case DDP_OPT_MULTICAST: *v = c->multicast; break;
+    case DDP_OPT_CE_STREAMS: *v = c->ce_streams; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;

@@ -42,6 +42,7 @@ struct P2PLaunch {
   float scale;                // fl(1/world)
   int64_t grad_rank_stride;   // emulation: byte distance between ranks' gradients
   uint32_t* err;              // device-visible error word (mapped pinned host memory)
+  void* mc;                   // NVLS: multicast address of the storage base (NULL otherwise)
 };
 
 // Several buckets launched together at world 1: slot k covers virtual elements
@@ -61,10 +62,22 @@ cudaError_t launch_pack(int dtype, const SlotView& sv, void* bucket, float scale
 cudaError_t launch_unpack(int dtype, const SlotView& sv, const void* bucket, int max_ctas,
                           cudaStream_t s);
 cudaError_t launch_p2p(int algo, int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
-// Copy-engine algorithm, SM part: grad = RNE(sum over the W slots, rank order);
-// slot q of element x at slot0 + q * stride_elems + x.
-cudaError_t launch_ce_reduce(int dtype, int world, const SlotView& sv, const void* slot0, int64_t stride_elems,
-                             int max_ctas, cudaStream_t s);
+// NVLS (NVSwitch multicast) two-shot: pack -> multimem.ld_reduce + multimem.st -> unpack.
+cudaError_t launch_nvls(int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
+// Copy-engine algorithm, SM part.  A list of gradients with their element
+// offsets inside a slot ("wire layout").
+struct CeView {
+  void* const* grad;
+  const int64_t* wire;
+  const int64_t* numel;
+  int32_t n;
+};
+// own_slot[wire_k + i] = grad_k[i] (raw) for the listed (small) gradients.
+cudaError_t launch_ce_gather(int dtype, const CeView& v, void* own_slot, int max_ctas, cudaStream_t s);
+// grad_k[i] = RNE( sum_q RNE(v_q * scale) ), rank order; v_rank = grad_k[i],
+// v_q = slot q (slot0 + q * stride_bytes) at wire_k + i.
+cudaError_t launch_ce_reduce(int dtype, int world, int rank, const CeView& v, const void* slot0,
+                             int64_t stride_bytes, float scale, int max_ctas, cudaStream_t s);
 // Locally-unused parameters (find_unused): copy src (library scratch holding the
 // average) -> dst (the caller's gradient) where global_used[param] > 0.
 struct UnusedView {

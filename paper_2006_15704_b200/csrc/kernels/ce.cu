@@ -1,12 +1,20 @@
 // ce.cu — the SM part of the copy-engine (CE) bucket allreduce.
 //
 // In the CE algorithm the NVLink traffic is moved by the copy engines
-// (cudaMemcpyAsync into the peers' slots) and ordered by stream memory
-// operations, so no SM spins or pushes while backward runs (overlap,
-// P:L184-L186).  What remains on the SMs is pack (pack.cu) and this
-// reduction, which sums the W slots of a bucket in rank order in fp32 and
-// writes the result straight into the gradients (fused unpack):
-//     grad_p[i] = RNE( sum_{q=0..W-1} slot_q[off_p + i] )      (oracle O-3b)
+// (cudaMemcpyAsync into the peers' slots, straight from .grad for large
+// gradients) and ordered by stream memory operations, so no SM spins or
+// pushes while backward runs (overlap).  The bucket is carried on
+// the wire in "wire layout": large gradients first, then the small ones,
+// each at a 64-element aligned wire offset.  What remains on the SMs:
+//
+//   ce_gather_kernel:  small gradients -> this rank's own slot (raw copy, so
+//                      one copy-engine transfer carries all of them);
+//   ce_reduce_kernel:  grad_p[i] = RNE( sum_{q=0..W-1} RNE(v_q[i] * fl(1/W)) )
+//                      in rank order, v_r = grad_p (own, raw), v_q = slot q at
+//                      the wire offset (raw, pushed by rank q) — the pack
+//                      scale of Alg. 1 L231-L232 applied on the fly per
+//                      operand, i.e. exactly oracle O-3b, written straight
+//                      into the gradients (fused unpack).
 #include "common.cuh"
 
 namespace b200ddp {
@@ -15,69 +23,154 @@ namespace {
 
 constexpr int64_t kTileBytes = (int64_t)kThreads * 16 * 4;
 
-template <typename T, int W, int MAXS>
-__global__ void __launch_bounds__(kThreads) reduce_slots_kernel(const __grid_constant__ SlotArgs<MAXS> sa,
-                                                                const T* __restrict__ slot0, int64_t stride) {
+template <int MAXS>
+struct CeArgs {
+  void* grad[MAXS];
+  int64_t wire[MAXS];     // element offset inside a slot
+  int64_t vo[MAXS + 1];   // virtual offsets: concatenation of the listed gradients
+  int32_t n;
+};
+
+template <int MAXS>
+__device__ __forceinline__ int find_v(const CeArgs<MAXS>& a, int64_t x) {
+  int lo = 0, hi = a.n - 1;
+  while (lo < hi) {
+    const int m = (lo + hi + 1) >> 1;
+    if (a.vo[m] <= x) lo = m; else hi = m - 1;
+  }
+  return lo;
+}
+
+template <typename T, int MAXS>
+__global__ void __launch_bounds__(kThreads) ce_gather_kernel(const __grid_constant__ CeArgs<MAXS> a,
+                                                             T* __restrict__ own_slot) {
   constexpr int64_t tile = kTileBytes / sizeof(T);
-  const T* src[W];
-#pragma unroll
-  for (int q = 0; q < W; ++q) src[q] = slot0 + q * stride;
-  const int64_t lo0 = sa.off[0], hi0 = sa.off[sa.n];
-  for (int64_t t = lo0 + (int64_t)blockIdx.x * tile; t < hi0; t += (int64_t)gridDim.x * tile)
-    walk_unpack<T, W, MAXS>(sa, t, min(t + tile, hi0), src, 0, 0);
+  const int64_t total = a.vo[a.n];
+  for (int64_t t = (int64_t)blockIdx.x * tile; t < total; t += (int64_t)gridDim.x * tile) {
+    const int64_t hi = min(t + tile, total);
+    for (int k = find_v(a, t); k < a.n && a.vo[k] < hi; ++k) {
+      const int64_t x0 = max(t, a.vo[k]), x1 = min(hi, a.vo[k + 1]);
+      if (x0 >= x1) continue;
+      const int64_t i0 = x0 - a.vo[k];
+      T* d[1] = {own_slot + a.wire[k] + i0};
+      const T* s[1] = {static_cast<const T*>(a.grad[k]) + i0};
+      cta_xfer<T, 1, 1, true, false>(d, s, x1 - x0, 1.0f);
+    }
+  }
 }
 
 template <typename T, int W, int MAXS>
-cudaError_t run(const SlotView& sv, int first, int n, const void* slot0, int64_t stride, int max_ctas,
-                cudaStream_t st) {
-  SlotArgs<MAXS> a;
-  a.n = n;
-  for (int k = 0; k < n; ++k) {
-    a.grad[k] = sv.grad[first + k];
-    a.off[k] = sv.off[first + k];
+__global__ void __launch_bounds__(kThreads) ce_reduce_kernel(const __grid_constant__ CeArgs<MAXS> a,
+                                                             const char* __restrict__ slot0, int64_t stride,
+                                                             int rank, float s) {
+  constexpr int64_t tile = kTileBytes / sizeof(T);
+  const int64_t total = a.vo[a.n];
+  for (int64_t t = (int64_t)blockIdx.x * tile; t < total; t += (int64_t)gridDim.x * tile) {
+    const int64_t hi = min(t + tile, total);
+    for (int k = find_v(a, t); k < a.n && a.vo[k] < hi; ++k) {
+      const int64_t x0 = max(t, a.vo[k]), x1 = min(hi, a.vo[k + 1]);
+      if (x0 >= x1) continue;
+      const int64_t i0 = x0 - a.vo[k];
+      T* g = static_cast<T*>(a.grad[k]) + i0;
+      T* d[1] = {g};
+      const T* src[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+        src[q] = q == rank ? g : reinterpret_cast<const T*>(slot0 + q * stride) + a.wire[k] + i0;
+      cta_xfer<T, W, 1, false, true, true>(d, src, x1 - x0, s);
+    }
   }
-  a.off[n] = sv.off[first + n];
-  const int64_t tile = kTileBytes / sizeof(T);
-  int64_t grid = (a.off[n] - a.off[0] + tile - 1) / tile;
-  if (grid > max_ctas) grid = max_ctas;
-  if (grid < 1) grid = 1;
-  reduce_slots_kernel<T, W, MAXS><<<(int)grid, kThreads, 0, st>>>(a, static_cast<const T*>(slot0), stride);
+}
+
+template <int MAXS>
+CeArgs<MAXS> make_args(const CeView& v, int first, int n) {
+  CeArgs<MAXS> a;
+  a.n = n;
+  int64_t pos = 0;
+  for (int k = 0; k < n; ++k) {
+    a.grad[k] = v.grad[first + k];
+    a.wire[k] = v.wire[first + k];
+    a.vo[k] = pos;
+    pos += v.numel[first + k];
+  }
+  a.vo[n] = pos;
+  return a;
+}
+
+int grid_for(int64_t elems, int64_t tile, int max_ctas) {
+  int64_t g = (elems + tile - 1) / tile;
+  if (g > max_ctas) g = max_ctas;
+  return g < 1 ? 1 : (int)g;
+}
+
+template <typename T, int W, int MAXS>
+cudaError_t run_reduce(const CeView& v, int first, int n, const void* slot0, int64_t stride, int rank,
+                       float s, int max_ctas, cudaStream_t st) {
+  const CeArgs<MAXS> a = make_args<MAXS>(v, first, n);
+  const int grid = grid_for(a.vo[n], kTileBytes / sizeof(T), max_ctas);
+  ce_reduce_kernel<T, W, MAXS><<<grid, kThreads, 0, st>>>(a, static_cast<const char*>(slot0), stride, rank, s);
   return cudaGetLastError();
 }
 
 template <typename T, int W>
-cudaError_t by_slots(const SlotView& sv, const void* slot0, int64_t stride, int max_ctas, cudaStream_t st) {
-  for (int first = 0; first < sv.n; first += kMaxSlotsPerLaunch) {
-    const int n = sv.n - first < kMaxSlotsPerLaunch ? sv.n - first : kMaxSlotsPerLaunch;
-    cudaError_t e = n <= 32    ? run<T, W, 32>(sv, first, n, slot0, stride, max_ctas, st)
-                    : n <= 256 ? run<T, W, 256>(sv, first, n, slot0, stride, max_ctas, st)
-                               : run<T, W, 1024>(sv, first, n, slot0, stride, max_ctas, st);
+cudaError_t reduce_by_slots(const CeView& v, const void* slot0, int64_t stride, int rank, float s, int max_ctas,
+                            cudaStream_t st) {
+  for (int first = 0; first < v.n; first += kMaxSlotsPerLaunch) {
+    const int n = v.n - first < kMaxSlotsPerLaunch ? v.n - first : kMaxSlotsPerLaunch;
+    cudaError_t e = n <= 32    ? run_reduce<T, W, 32>(v, first, n, slot0, stride, rank, s, max_ctas, st)
+                    : n <= 256 ? run_reduce<T, W, 256>(v, first, n, slot0, stride, rank, s, max_ctas, st)
+                               : run_reduce<T, W, 1024>(v, first, n, slot0, stride, rank, s, max_ctas, st);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
 }
 
 template <typename T>
-cudaError_t by_world(int world, const SlotView& sv, const void* slot0, int64_t stride, int max_ctas,
-                     cudaStream_t st) {
+cudaError_t reduce_by_world(int world, const CeView& v, const void* slot0, int64_t stride, int rank, float s,
+                            int max_ctas, cudaStream_t st) {
   switch (world) {
-    case 2: return by_slots<T, 2>(sv, slot0, stride, max_ctas, st);
-    case 3: return by_slots<T, 3>(sv, slot0, stride, max_ctas, st);
-    case 4: return by_slots<T, 4>(sv, slot0, stride, max_ctas, st);
-    case 5: return by_slots<T, 5>(sv, slot0, stride, max_ctas, st);
-    case 6: return by_slots<T, 6>(sv, slot0, stride, max_ctas, st);
-    case 7: return by_slots<T, 7>(sv, slot0, stride, max_ctas, st);
-    case 8: return by_slots<T, 8>(sv, slot0, stride, max_ctas, st);
+    case 2: return reduce_by_slots<T, 2>(v, slot0, stride, rank, s, max_ctas, st);
+    case 3: return reduce_by_slots<T, 3>(v, slot0, stride, rank, s, max_ctas, st);
+    case 4: return reduce_by_slots<T, 4>(v, slot0, stride, rank, s, max_ctas, st);
+    case 5: return reduce_by_slots<T, 5>(v, slot0, stride, rank, s, max_ctas, st);
+    case 6: return reduce_by_slots<T, 6>(v, slot0, stride, rank, s, max_ctas, st);
+    case 7: return reduce_by_slots<T, 7>(v, slot0, stride, rank, s, max_ctas, st);
+    case 8: return reduce_by_slots<T, 8>(v, slot0, stride, rank, s, max_ctas, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
+template <typename T, int MAXS>
+cudaError_t run_gather(const CeView& v, int first, int n, void* own_slot, int max_ctas, cudaStream_t st) {
+  const CeArgs<MAXS> a = make_args<MAXS>(v, first, n);
+  const int grid = grid_for(a.vo[n], kTileBytes / sizeof(T), max_ctas);
+  ce_gather_kernel<T, MAXS><<<grid, kThreads, 0, st>>>(a, static_cast<T*>(own_slot));
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t gather(const CeView& v, void* own_slot, int max_ctas, cudaStream_t st) {
+  for (int first = 0; first < v.n; first += kMaxSlotsPerLaunch) {
+    const int n = v.n - first < kMaxSlotsPerLaunch ? v.n - first : kMaxSlotsPerLaunch;
+    cudaError_t e = n <= 32    ? run_gather<T, 32>(v, first, n, own_slot, max_ctas, st)
+                    : n <= 256 ? run_gather<T, 256>(v, first, n, own_slot, max_ctas, st)
+                               : run_gather<T, 1024>(v, first, n, own_slot, max_ctas, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace
 
-cudaError_t launch_ce_reduce(int dtype, int world, const SlotView& sv, const void* slot0, int64_t stride_elems,
-                             int max_ctas, cudaStream_t s) {
-  return dtype == 0 ? by_world<float>(world, sv, slot0, stride_elems, max_ctas, s)
-                    : by_world<__nv_bfloat16>(world, sv, slot0, stride_elems, max_ctas, s);
+cudaError_t launch_ce_gather(int dtype, const CeView& v, void* own_slot, int max_ctas, cudaStream_t s) {
+  if (v.n == 0) return cudaSuccess;
+  return dtype == 0 ? gather<float>(v, own_slot, max_ctas, s) : gather<__nv_bfloat16>(v, own_slot, max_ctas, s);
+}
+
+cudaError_t launch_ce_reduce(int dtype, int world, int rank, const CeView& v, const void* slot0,
+                             int64_t stride_bytes, float scale, int max_ctas, cudaStream_t s) {
+  return dtype == 0 ? reduce_by_world<float>(world, v, slot0, stride_bytes, rank, scale, max_ctas, s)
+                    : reduce_by_world<__nv_bfloat16>(world, v, slot0, stride_bytes, rank, scale, max_ctas, s);
 }
 
 }  // namespace b200ddp

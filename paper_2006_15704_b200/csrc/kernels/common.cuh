@@ -89,7 +89,10 @@ template <> struct Elem<__nv_bfloat16> {
 // (data written by peers inside the kernel).  NS / ND are compile-time so the
 // pointer and value arrays live in registers; U vectors per source are kept
 // in flight per thread (U * NS >= 4).
-template <typename T, int NS, int ND, bool SRC_NC, bool SCALE>
+// EACH (with SCALE): every operand is scaled and rounded to T BEFORE the sum,
+//   y = RNE_T( sum_k RNE_T(src_k[i] * s) )        (oracle O-3b written out),
+// so raw gradients can be reduced with the 1/W of pack applied on the fly.
+template <typename T, int NS, int ND, bool SRC_NC, bool SCALE, bool EACH = false>
 __device__ __forceinline__ void cta_xfer(T* const (&dst)[ND], const T* const (&src)[NS], int64_t n,
                                          float s) {
   using E = Elem<T>;
@@ -105,11 +108,13 @@ __device__ __forceinline__ void cta_xfer(T* const (&dst)[ND], const T* const (&s
   for (int k = 0; k < NS; ++k) mis |= (reinterpret_cast<uintptr_t>(src[k]) & 15) ^ a0;
 
   auto ld1 = [&](const T* p) -> float { return E::to_f(SRC_NC ? __ldg(p) : __ldcg(p)); };
+  auto each = [&](float x) -> float { return E::to_f(E::from_f(__fmul_rn(x, s))); };
   auto scalar = [&](int64_t i) {
     float acc = ld1(src[0] + i);
+    if (EACH) acc = each(acc);
 #pragma unroll
-    for (int k = 1; k < NS; ++k) acc = __fadd_rn(acc, ld1(src[k] + i));
-    if (SCALE) acc = __fmul_rn(acc, s);
+    for (int k = 1; k < NS; ++k) acc = __fadd_rn(acc, EACH ? each(ld1(src[k] + i)) : ld1(src[k] + i));
+    if (SCALE && !EACH) acc = __fmul_rn(acc, s);
     const T y = E::from_f(acc);
 #pragma unroll
     for (int j = 0; j < ND; ++j) dst[j][i] = y;
@@ -126,13 +131,17 @@ __device__ __forceinline__ void cta_xfer(T* const (&dst)[ND], const T* const (&s
   auto vec = [&](int64_t v, const uint4 (&in)[NS]) {
     float acc[8], f[8];
     E::unpack(in[0], acc);
+    if (EACH) {
+#pragma unroll
+      for (int e = 0; e < VE; ++e) acc[e] = each(acc[e]);
+    }
 #pragma unroll
     for (int k = 1; k < NS; ++k) {
       E::unpack(in[k], f);
 #pragma unroll
-      for (int e = 0; e < VE; ++e) acc[e] = __fadd_rn(acc[e], f[e]);
+      for (int e = 0; e < VE; ++e) acc[e] = __fadd_rn(acc[e], EACH ? each(f[e]) : f[e]);
     }
-    if (SCALE) {
+    if (SCALE && !EACH) {
 #pragma unroll
       for (int e = 0; e < VE; ++e) acc[e] = __fmul_rn(acc[e], s);
     }

@@ -66,13 +66,24 @@ class GradReducer:
             self.storage_bytes = L.ddp_storage_bytes(self.ctx)
             self.comm_stream = comm_stream or torch.cuda.Stream(device=self.device, priority=-1)
             nccl_id = L.ddp_get_nccl_id() if self.rank == 0 else None
+            mc = 0
             if self.world > 1:
                 nccl_id = _broadcast_id(nccl_id, self.rank, group, self.device)
-                self._storage, peers = self._symmetric_storage()
+                self._storage, peers, mc = self._symmetric_storage()
+                want = (options or {}).get(L.OPT_MULTICAST)
+                ok = self._all_agree(mc != 0)          # NVLS only if every rank has multicast
+                if want and not ok:
+                    raise RuntimeError("OPT_MULTICAST requested but NVSwitch multicast is unavailable")
+                if want is None and ok:
+                    L.ddp_set_option(self.ctx, L.OPT_MULTICAST, 1)
+                    assert L.ddp_storage_bytes(self.ctx) <= self.storage_bytes
+                if not L.ddp_get_option(self.ctx, L.OPT_MULTICAST):
+                    mc = 0
             else:
                 self._storage = torch.empty(self.storage_bytes, dtype=torch.uint8, device=self.device)
                 peers = [self._storage.data_ptr()]
-            L.ddp_bind_device(self.ctx, self.device.index, nccl_id, self.comm_stream.cuda_stream, peers)
+            self.multicast = bool(mc)
+            L.ddp_bind_device(self.ctx, self.device.index, nccl_id, self.comm_stream.cuda_stream, peers, mc)
         except Exception:
             L.ddp_destroy(self.ctx)
             self.ctx = None
@@ -85,7 +96,15 @@ class GradReducer:
         base = h.buffer_ptrs[self.rank]
         delta = t.data_ptr() - base
         self._symm_handle = h
-        return t, [int(p) + delta for p in h.buffer_ptrs]
+        mc = 0
+        if getattr(h, "has_multicast_support", False) and h.multicast_ptr:
+            mc = int(h.multicast_ptr) + delta
+        return t, [int(p) + delta for p in h.buffer_ptrs], mc
+
+    def _all_agree(self, flag: bool) -> bool:
+        t = torch.tensor([1 if flag else 0], dtype=torch.int32, device=self.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return bool(t.item())
 
     # ---- introspection -------------------------------------------------------
     @property
