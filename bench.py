@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--pack-ctas", type=int, default=0)
     ap.add_argument("--stage-kib", type=int, default=0)
     ap.add_argument("--ce-streams", type=int, default=0)
+    ap.add_argument("--nccl-comms", type=int, default=0, help="round-robin NCCL communicators (P:L535)")
     ap.add_argument("--exposed-model", default="resnet50", choices=["none", "resnet50", "bert_large"],
                     help="real-model backward for the exposed-time measurement")
     ap.add_argument("--exposed-batch", type=int, default=0)
@@ -218,6 +219,8 @@ def run_ours(a):
         opts[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
     if a.ce_streams:
         opts[L.OPT_CE_STREAMS] = a.ce_streams
+    if a.nccl_comms:
+        opts[L.OPT_NCCL_COMMS] = a.nccl_comms
     if a.oneshot_max >= 0:
         opts[L.OPT_P2P_ONESHOT_MAX] = a.oneshot_max
     if a.twoshot_max >= 0:
@@ -293,6 +296,8 @@ def run_ours(a):
     S_tot = sum(bnumel) * esize
     # our kernel launches per step (NCCL's own kernels excluded)
     launches_per_step = sum(prof[k][1] for k in ("pack", "unpack", "p2p_fused", "ce_reduce")) / kprof_steps
+    if "push" in red.bucket_algos():   # the push kernels are ours too (copy-engine transfers are not kernels)
+        launches_per_step += prof["ce_copy"][1] / kprof_steps
 
     # dominant kernel roofline: algorithmic bytes per launch / measured launch time
     peak_hbm, peak_src = measured_peaks()
@@ -304,7 +309,7 @@ def run_ours(a):
             for s_ in range(L.ddp_bucket_info(red.ctx, b)[1]):
                 p, _ = L.ddp_bucket_slot(red.ctx, b, s_)
                 small += ns[p] * esize if ns[p] * esize < (1 << 20) else 0
-    by = {x: sum(n * esize for n, y in zip(bnumel, algos) if y == x) for x in ("nccl", "oneshot", "twoshot", "ce", "nvls")}
+    by = {x: sum(n * esize for n, y in zip(bnumel, algos) if y == x) for x in ("nccl", "oneshot", "twoshot", "ce", "nvls", "push")}
 
     def kind_bytes(kind):
         """(algorithmic bytes per step, bound, rule) of one profile kind."""
@@ -319,9 +324,11 @@ def run_ours(a):
                     + by["nvls"] * (1 + 1 / world), "nvlink",
                     "NVLink bytes per direction: one-shot (W-1)S, two-shot 2(W-1)/W S, NVLS (1+1/W)S")
         if kind == "ce_copy":
-            return by["ce"] * (world - 1), "nvlink", "copy-engine NVLink bytes per direction (W-1)S"
+            return ((by["ce"] + by["push"]) * (world - 1), "nvlink",
+                    "NVLink bytes per direction (W-1)S (copy engines / push kernel)")
         if kind == "ce_reduce":
-            return by["ce"] * (world + 1), "hbm", "(W+1) x bucket bytes (W operands read, .grad written)"
+            return ((by["ce"] + by["push"]) * (world + 1), "hbm",
+                    "(W+1) x bucket bytes (W operands read, .grad written)")
         return 2 * (world - 1) / world * by["nccl"], "nvlink", "ring 2(W-1)/W x bucket bytes"
 
     def roof_of(kind):
@@ -619,6 +626,8 @@ def _opts(a):
         o[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
     if a.ce_streams:
         o[L.OPT_CE_STREAMS] = a.ce_streams
+    if a.nccl_comms:
+        o[L.OPT_NCCL_COMMS] = a.nccl_comms
     if a.oneshot_max >= 0:
         o[L.OPT_P2P_ONESHOT_MAX] = a.oneshot_max
     if a.twoshot_max >= 0:
@@ -669,7 +678,8 @@ def allreduce_sweep(a, rank, world, local, dev, opts):
     tdt = torch.float32 if a.dtype == "fp32" else torch.bfloat16
     esize = 4 if a.dtype == "fp32" else 2
     stream = torch.cuda.current_stream(dev)
-    algos = [L.ALGO_AUTO, L.ALGO_NCCL, L.ALGO_ONESHOT, L.ALGO_TWOSHOT] + ([L.ALGO_CE, L.ALGO_NVLS] if world > 1 else [])
+    algos = [L.ALGO_AUTO, L.ALGO_NCCL, L.ALGO_ONESHOT, L.ALGO_TWOSHOT] + (
+        [L.ALGO_CE, L.ALGO_NVLS, L.ALGO_PUSH] if world > 1 else [])
     sizes = [4 << 10, 64 << 10, 256 << 10, 1 << 20, 4 << 20, 16 << 20, 25 << 20, 64 << 20, 256 << 20]
     res = []
 

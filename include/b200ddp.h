@@ -74,7 +74,8 @@ enum {
   DDP_OPT_DRY_RUN = 5,          /* 1: protocol only, no device work (host tests; CREATED only) */
   DDP_OPT_PROFILE = 6,          /* 1: time every device launch with CUDA events */
   DDP_OPT_ALGO = 7,             /* force the bucket allreduce: 0 auto, 1 NCCL, 2 one-shot, 3 two-shot,
-                                   4 copy-engine one-shot (world > 1), 5 NVLS (needs MULTICAST) */
+                                   4 copy-engine one-shot (world > 1), 5 NVLS (needs MULTICAST),
+                                   6 SM push + stream-ordered reduce (world > 1) */
   DDP_OPT_PACK_CTAS = 8,        /* max CTAs of pack/unpack kernels and of P2P kernels at world 1 */
   DDP_OPT_P2P_STAGE_BYTES = 9,  /* 0 (default): one pipeline stage per CTA chunk; else split each
                                    CTA chunk into stages of this many bytes (one sync per stage) */
@@ -85,8 +86,11 @@ enum {
   DDP_OPT_MULTICAST = 11,       /* 1: the caller will pass a multicast (NVLS) address of the storage
                                    to ddp_bind_device, enabling DDP_ALGO_NVLS; CREATED only.  Every
                                    rank must agree.  Never increases ddp_storage_bytes */
-  DDP_OPT_CE_STREAMS = 12       /* copy-engine algorithm: number of streams its peer copies are
+  DDP_OPT_CE_STREAMS = 12,      /* copy-engine algorithm: number of streams its peer copies are
                                    spread over (1..16, default 4); before binding only */
+  DDP_OPT_NCCL_COMMS = 13       /* round-robin process groups (Fig. 12 "rrx"): NCCL
+                                   bucket b runs on communicator b mod k (split off the first with
+                                   ncclCommSplit) and its own stream; 1..8, default 1; before binding */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.
@@ -98,9 +102,13 @@ enum {
  *            stream.  Frees the SMs for the overlapped backward.
  *   NVLS:    one fused sm_100a kernel: pack -> multimem.ld_reduce / multimem.st through the
  *            NVSwitch multicast address ((1+1/W) S NVLink bytes per direction) -> unpack.
- *            Needs DDP_OPT_MULTICAST; otherwise resolves to TWOSHOT. */
+ *            Needs DDP_OPT_MULTICAST; otherwise resolves to TWOSHOT.
+ *   PUSH:    as CE, but the transfer is one sm_100a kernel per bucket that reads every gradient
+ *            once and stores it into every peer's slot (no waiting inside kernels; the ready /
+ *            consumed flags are stream memory operations), so bucket b+1's push overlaps bucket
+ *            b's reduction on the second stream. */
 enum { DDP_ALGO_AUTO = 0, DDP_ALGO_NCCL = 1, DDP_ALGO_ONESHOT = 2, DDP_ALGO_TWOSHOT = 3, DDP_ALGO_CE = 4,
-       DDP_ALGO_NVLS = 5 };
+       DDP_ALGO_NVLS = 5, DDP_ALGO_PUSH = 6 };
 
 /* ---- construction (host only, deterministic, touches no GPU) -------------
  * Bucket assignment (Alg. 1 "allocate parameters to buckets in the
@@ -115,6 +123,16 @@ enum { DDP_ALGO_AUTO = 0, DDP_ALGO_NCCL = 1, DDP_ALGO_ONESHOT = 2, DDP_ALGO_TWOS
 ddp_status_t ddp_create(const int64_t* param_numel, int32_t n_params, int32_t dtype,
                         int64_t bucket_cap_bytes, int32_t world, int32_t rank, ddp_ctx_t** out);
 void ddp_destroy(ddp_ctx_t* ctx); /* NULL-safe; aborts the NCCL comm if poisoned */
+/* ddp_create_ordered: as ddp_create, but the bucketing scan visits the
+ * parameters in scan_order[n_params] (a permutation) instead of reverse
+ * registration order — the "gradient order prediction" of PAPER.md §6.2.1
+ * (L563-L565): trace the backward order (ddp_ready_order) and rebuild the
+ * parameter-to-bucket map, rarely, with one order agreed by every rank (e.g.
+ * rank 0's, broadcast).  NULL = reverse registration order (= ddp_create).
+ * Errors: as ddp_create; DDP_ERR_INVALID_ARG if scan_order is not a permutation. */
+ddp_status_t ddp_create_ordered(const int64_t* param_numel, int32_t n_params, const int32_t* scan_order,
+                                int32_t dtype, int64_t bucket_cap_bytes, int32_t world, int32_t rank,
+                                ddp_ctx_t** out);
 
 /* ---- introspection: the bit-exact mapping contract ---------------------- */
 int32_t ddp_num_buckets(const ddp_ctx_t* ctx); /* -1 if ctx is NULL */
@@ -209,8 +227,9 @@ ddp_status_t ddp_launch_trace(const ddp_ctx_t* ctx, int32_t* buckets, int32_t* t
                               int32_t cap, int32_t* n);
 /* With DDP_OPT_PROFILE=1: synchronizes the recorded events and returns the
  * summed device milliseconds and launch counts since the last read, per kind
- * [0]=pack [1]=NCCL allreduce [2]=unpack [3]=fused P2P kernel (incl. world-1 group)
- * [4]=copy-engine pushes [5]=copy-engine reduce kernel; then clears. */
+ * [0]=pack (CE: gather of small gradients) [1]=NCCL allreduce [2]=unpack [3]=fused P2P / NVLS
+ * kernel (incl. world-1 group) [4]=CE / PUSH transfer (copy engines or the push kernel)
+ * [5]=CE / PUSH reduce kernel; then clears. */
 ddp_status_t ddp_profile_read(ddp_ctx_t* ctx, double ms[6], int64_t launches[6]);
 /* With DDP_OPT_PROFILE=1: per device launch since the last read (in launch
  * order), its kind (as above), the time its bucket(s) became ready on the
@@ -219,6 +238,17 @@ ddp_status_t ddp_profile_read(ddp_ctx_t* ctx, double ms[6], int64_t launches[6])
  * timeline).  *n receives the count; at most cap entries are written; clears. */
 ddp_status_t ddp_profile_timeline(ddp_ctx_t* ctx, int32_t cap, int32_t* kinds, double* ready_ms,
                                   double* start_ms, double* end_ms, int32_t* n);
+/* Parameter indices in the order their ready signals (ddp_grad_ready /
+ * ddp_mark_unused) arrived in the most recent finished pass (the open one if a
+ * pass is open) — the trace for ddp_create_ordered.  *n receives the count. */
+ddp_status_t ddp_ready_order(const ddp_ctx_t* ctx, int32_t* out, int32_t cap, int32_t* n);
+/* Alg. 1 constructor (L214-L215): "broadcast net states to other processes".
+ * Broadcasts n device buffers (bytes[i] bytes each, in place) from rank root over
+ * the library's communicator, as one NCCL group on `stream`.  Collective: every
+ * rank calls it with the same sizes.  Legal between passes on a bound context.
+ * Errors: DDP_ERR_STATE, DDP_ERR_INVALID_ARG, DDP_ERR_NCCL. */
+ddp_status_t ddp_broadcast(ddp_ctx_t* ctx, void* const* bufs, const int64_t* bytes, int32_t n, int32_t root,
+                           void* stream);
 /* Checks the device-side error word (P2P barrier timeout). */
 ddp_status_t ddp_check_device_errors(ddp_ctx_t* ctx);
 const char* ddp_last_error(void);

@@ -19,6 +19,7 @@ average     O-3  fp64 average; O-3b bit-faithful fp32 average;
                  full pack -> allreduce -> unpack simulation    (pinned)
 mlp         O-4  toy MLP, fp64 manual backprop; equivalence     (pinned)
 nosync      O-5  no_sync accumulation                            (pinned)
+unused      O-7  globally unused parameters (find_unused)        (pinned)
 cpu_baseline O-6 timing harness around ``average.simulate_ddp_sync``
                  (timing only; no new arithmetic)
 """

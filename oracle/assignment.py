@@ -20,7 +20,7 @@ an oversized parameter sits alone.  C-5 "MB" = MiB.  C-6 tight packing
 from __future__ import annotations
 
 from dataclasses import dataclass
-from typing import List, Sequence, Tuple
+from typing import List, Optional, Sequence, Tuple
 
 MIB = 1 << 20
 
@@ -37,8 +37,11 @@ class Assignment:
         return len(self.buckets)
 
 
-def assign_buckets(numel: Sequence[int], elem_size: int, cap_bytes: int) -> Assignment:
-    """Greedy scan p = n-1 ... 0 (reverse registration order, Alg. 1).
+def assign_buckets(numel: Sequence[int], elem_size: int, cap_bytes: int,
+                   order: Optional[Sequence[int]] = None) -> Assignment:
+    """Greedy scan p = n-1 ... 0 (reverse registration order, Alg. 1), or
+    over ``order`` when given (the traced backward order of PAPER.md L563-L565,
+    "gradient order prediction": the map is rebuilt from the observed order).
 
     A bucket is closed before the parameter that would push its byte size over
     ``cap_bytes`` (unless the bucket is empty); each parameter is appended at
@@ -48,11 +51,14 @@ def assign_buckets(numel: Sequence[int], elem_size: int, cap_bytes: int) -> Assi
         raise ValueError("need at least one parameter")
     if cap_bytes < 0 or elem_size <= 0 or any(int(x) < 1 for x in numel):
         raise ValueError("invalid arguments")
+    scan = list(range(n - 1, -1, -1)) if order is None else [int(p) for p in order]
+    if sorted(scan) != list(range(n)):
+        raise ValueError("order must be a permutation of the parameters")
     buckets: List[List[Tuple[int, int]]] = []
     sizes: List[int] = []
     cur: List[Tuple[int, int]] = []
     cur_numel = 0
-    for p in range(n - 1, -1, -1):
+    for p in scan:
         if cur and (cur_numel + numel[p]) * elem_size > cap_bytes:
             buckets.append(cur)
             sizes.append(cur_numel)

@@ -23,10 +23,11 @@ STATUS_NAMES = ["OK", "INVALID_ARG", "STATE", "DUPLICATE", "INCOMPLETE", "CUDA",
                 "POISONED", "TIMEOUT", "UNSUPPORTED"]
 FP32, BF16 = 0, 1
 OPT_OVERLAP, OPT_P2P_ONESHOT_MAX, OPT_P2P_TWOSHOT_MAX, OPT_COMM_CTAS, OPT_DRY_RUN, OPT_PROFILE, \
-    OPT_ALGO, OPT_PACK_CTAS, OPT_P2P_STAGE_BYTES, OPT_FIND_UNUSED, OPT_MULTICAST, OPT_CE_STREAMS = range(1, 13)
-ALGO_AUTO, ALGO_NCCL, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_CE, ALGO_NVLS = range(6)
+    OPT_ALGO, OPT_PACK_CTAS, OPT_P2P_STAGE_BYTES, OPT_FIND_UNUSED, OPT_MULTICAST, OPT_CE_STREAMS, \
+    OPT_NCCL_COMMS = range(1, 14)
+ALGO_AUTO, ALGO_NCCL, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_CE, ALGO_NVLS, ALGO_PUSH = range(7)
 ALGO_NAMES = {ALGO_NCCL: "nccl", ALGO_ONESHOT: "oneshot", ALGO_TWOSHOT: "twoshot", ALGO_CE: "ce",
-              ALGO_NVLS: "nvls"}
+              ALGO_NVLS: "nvls", ALGO_PUSH: "push"}
 PROFILE_KINDS = ("pack", "nccl_allreduce", "unpack", "p2p_fused", "ce_copy", "ce_reduce")
 
 
@@ -43,6 +44,10 @@ _SIGS = {
     "ddp_create": (C.c_int, [C.POINTER(C.c_int64), C.c_int32, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
                              C.POINTER(_P)]),
     "ddp_destroy": (None, [_P]),
+    "ddp_create_ordered": (C.c_int, [C.POINTER(C.c_int64), C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.c_int64,
+                                     C.c_int32, C.c_int32, C.POINTER(_P)]),
+    "ddp_ready_order": (C.c_int, [_P, C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32)]),
+    "ddp_broadcast": (C.c_int, [_P, C.POINTER(_P), C.POINTER(C.c_int64), C.c_int32, C.c_int32, _P]),
     "ddp_num_buckets": (C.c_int32, [_P]),
     "ddp_bucket_info": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]),
     "ddp_bucket_slot": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
@@ -99,6 +104,30 @@ def ddp_create(param_numel: Sequence[int], dtype: int, bucket_cap_bytes: int, wo
     out = _P()
     _check(lib().ddp_create(arr, len(param_numel), dtype, int(bucket_cap_bytes), world, rank, C.byref(out)))
     return out.value
+
+
+def ddp_create_ordered(param_numel: Sequence[int], scan_order: Optional[Sequence[int]], dtype: int,
+                       bucket_cap_bytes: int, world: int, rank: int) -> int:
+    arr = (C.c_int64 * len(param_numel))(*[int(x) for x in param_numel])
+    order = None if scan_order is None else (C.c_int32 * len(scan_order))(*[int(x) for x in scan_order])
+    out = _P()
+    _check(lib().ddp_create_ordered(arr, len(param_numel), order, dtype, int(bucket_cap_bytes), world, rank,
+                                    C.byref(out)))
+    return out.value
+
+
+def ddp_ready_order(ctx: int) -> List[int]:
+    n = C.c_int32()
+    _check(lib().ddp_ready_order(ctx, None, 0, C.byref(n)))
+    buf = (C.c_int32 * max(1, n.value))()
+    _check(lib().ddp_ready_order(ctx, buf, n.value, C.byref(n)))
+    return [buf[i] for i in range(n.value)]
+
+
+def ddp_broadcast(ctx: int, ptrs: Sequence[int], nbytes: Sequence[int], root: int, stream: int) -> None:
+    p = (_P * max(1, len(ptrs)))(*ptrs)
+    b = (C.c_int64 * max(1, len(nbytes)))(*[int(x) for x in nbytes])
+    _check(lib().ddp_broadcast(ctx, p, b, len(ptrs), root, stream))
 
 
 def ddp_destroy(ctx: int) -> None:

@@ -84,6 +84,7 @@ struct ddp_ctx {
   int32_t world = 1, rank = 0, dtype = 0, esize = 4;
   int64_t cap = 0;
   std::vector<int64_t> numel;
+  std::vector<int32_t> scan;  // bucketing scan order (default: reverse registration)
   std::vector<Bucket> buckets;
   std::vector<int32_t> p_bucket, p_slot;
   std::vector<int64_t> p_off;
@@ -92,7 +93,7 @@ struct ddp_ctx {
   // NVLink bytes as two-shot with one sync instead of two; world > 2: <= 512 KiB)
   int64_t overlap = 1, oneshot_max = -1, twoshot_max = INT64_MAX, comm_ctas = 64,
           dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 8, stage_bytes = 0,
-          find_unused = 0, multicast = 0, ce_streams = 4;
+          find_unused = 0, multicast = 0, ce_streams = 4, nccl_comms = 1;
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
           stage1_stride = 0, ce_flags_off = 0, bitmap_off = 0, scratch_off = 0, storage_bytes = 0;
@@ -128,10 +129,17 @@ struct ddp_ctx {
   std::vector<int32_t> pending;
   int32_t cursor = 0, n_ready = 0;
   std::vector<std::pair<int32_t, int32_t>> trace, last_trace;
+  std::vector<int32_t> order, last_order;  // ready-signal order of the open / last finished pass
   // device state
   int device = -1;
   cudaStream_t comm = nullptr;
   ncclComm_t nccl = nullptr;
+  // round-robin process groups: NCCL bucket b runs on communicator
+  // b mod k and its own stream (index 0 = the main communicator / comm stream)
+  std::vector<ncclComm_t> rr_comm;
+  std::vector<cudaStream_t> rr_stream;
+  std::vector<cudaEvent_t> rr_done;
+  std::vector<uint8_t> rr_used;
   void* storage[kMaxWorld] = {};
   void* mc = nullptr;  // NVLS multicast address of the storage base
   int64_t grad_rank_stride = 0;
@@ -179,7 +187,8 @@ void assign(ddp_ctx* c) {
   const int n = (int)c->numel.size();
   c->buckets.clear();
   Bucket cur;
-  for (int p = n - 1; p >= 0; --p) {
+  for (int i = 0; i < n; ++i) {
+    const int p = c->scan[i];
     if (!cur.params.empty() && (cur.numel + c->numel[p]) * c->esize > c->cap) {
       c->buckets.push_back(std::move(cur));
       cur = Bucket();
@@ -209,7 +218,7 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   int a;
   if (c->algo != DDP_ALGO_AUTO) {
     a = (int)c->algo;
-    if (c->world == 1 && (a == DDP_ALGO_CE || a == DDP_ALGO_NVLS)) a = DDP_ALGO_ONESHOT;
+    if (c->world == 1 && (a == DDP_ALGO_CE || a == DDP_ALGO_NVLS || a == DDP_ALGO_PUSH)) a = DDP_ALGO_ONESHOT;
     if (a == DDP_ALGO_NVLS && !c->multicast) a = DDP_ALGO_TWOSHOT;
   } else if (c->world == 1) {
     a = DDP_ALGO_ONESHOT;
@@ -220,7 +229,7 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   } else {
     a = DDP_ALGO_NCCL;
   }
-  if ((a == DDP_ALGO_ONESHOT || a == DDP_ALGO_TWOSHOT || a == DDP_ALGO_CE || a == DDP_ALGO_NVLS) &&
+  if (a != DDP_ALGO_NCCL &&
       (int)bk.params.size() > kMaxSlotsPerLaunch)
     a = DDP_ALGO_NCCL;
   return a;
@@ -279,7 +288,7 @@ void plan(ddp_ctx* c) {
     bk.ce_stride = 0;
     bk.ce_wire.clear();
     bk.ce_direct.clear();
-    if (bk.algo != DDP_ALGO_CE) continue;
+    if (bk.algo != DDP_ALGO_CE && bk.algo != DDP_ALGO_PUSH) continue;
     const size_t ns = bk.params.size();
     bk.ce_wire.assign(ns, 0);
     bk.ce_direct.assign(ns, 0);
@@ -288,7 +297,7 @@ void plan(ddp_ctx* c) {
       if (pass == 1) bk.ce_small0 = w;
       for (size_t k = 0; k < ns; ++k) {
         const int64_t n = bk.off[k + 1] - bk.off[k];
-        const bool direct = n * c->esize >= kCeDirectBytes;
+        const bool direct = bk.algo == DDP_ALGO_CE && n * c->esize >= kCeDirectBytes;
         if (direct != (pass == 0)) continue;
         bk.ce_direct[k] = direct;
         bk.ce_wire[k] = w;
@@ -380,10 +389,11 @@ ddp_status_t launch_ce(ddp_ctx* c, int b) {
   char* own_slot = mine + bk.ce_off + r * bk.ce_stride;
   const uint32_t v = ++bk.ce_count;
   const size_t ns = bk.params.size();
+  const bool push = bk.algo == DDP_ALGO_PUSH;
   c->ce_grad.clear();
   c->ce_wire.clear();
   c->ce_numel.clear();
-  for (size_t k = 0; k < ns; ++k) {
+  for (size_t k = 0; k < ns && !push; ++k) {
     if (bk.ce_direct[k]) continue;
     c->ce_grad.push_back(bk.grads[k]);
     c->ce_wire.push_back(bk.ce_wire[k]);
@@ -402,11 +412,23 @@ ddp_status_t launch_ce(ddp_ctx* c, int b) {
   if (v > 1)
     for (int i = 1; i < W; ++i)
       if (ddp_status_t st = ce_wait(c, c->comm, ce_flag(c, r, 1, b, (r + i) % W), v - 1)) return st;
+  if (push) {  // SM push: one kernel reads each gradient once and stores it into every peer
+    void* peers[kMaxWorld];
+    for (int i = 1; i < W; ++i)
+      peers[i - 1] = static_cast<char*>(c->storage[(r + i) % W]) + bk.ce_off + r * bk.ce_stride;
+    c->ce_grad.assign(bk.grads.begin(), bk.grads.end());
+    c->ce_wire.assign(bk.ce_wire.begin(), bk.ce_wire.end());
+    for (size_t k = 0; k < ns; ++k) c->ce_numel.push_back(bk.off[k + 1] - bk.off[k]);
+    const CeView pv{c->ce_grad.data(), c->ce_wire.data(), c->ce_numel.data(), (int32_t)ns};
+    prof_begin(c, 4);
+    CUDA_TRY(c, launch_ce_push(c->dtype, pv, peers, W - 1, (int)std::min<int64_t>(c->comm_ctas, 148), c->comm));
+    prof_end(c);
+  }
   // Copies spread over the copy streams (each transfer carries a few us of fixed
   // latency; independent streams let several copy engines overlap it), the
   // largest-first into the least loaded stream.
-  const int K = (int)c->ce_cp.size();
-  prof_begin(c, 4);
+  const int K = push ? 0 : (int)c->ce_cp.size();
+  if (!push) prof_begin(c, 4);
   CUDA_TRY(c, cudaEventRecord(c->ce_go[b], c->comm));
   int64_t load[16] = {};
   bool used[16] = {};
@@ -440,7 +462,7 @@ ddp_status_t launch_ce(ddp_ctx* c, int b) {
     CUDA_TRY(c, cudaEventRecord(e, c->ce_cp[q]));
     CUDA_TRY(c, cudaStreamWaitEvent(c->comm, e, 0));
   }
-  prof_end(c);
+  if (!push) prof_end(c);
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
     if (ddp_status_t st = ce_write(c, c->comm, ce_flag(c, j, 0, b, r), v)) return st;
@@ -473,19 +495,23 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   const SlotView sv{bk.off.data(), bk.grads.data(), (int32_t)bk.params.size()};
   const float scale = 1.0f / (float)c->world;  // fl(1/W), reading C-2
   char* mine = static_cast<char*>(c->storage[c->rank]);
-  if (bk.algo == DDP_ALGO_CE) return launch_ce(c, b);
+  if (bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH) return launch_ce(c, b);
   if (bk.algo == DDP_ALGO_NCCL) {
     void* buf = mine + bk.byte_off;
-    prof_begin(c, 0);
-    CUDA_TRY(c, launch_pack(c->dtype, sv, buf, scale, (int)c->pack_ctas, c->comm));
-    prof_end(c);
-    prof_begin(c, 1);
+    const size_t k = c->rr_comm.empty() ? 0 : (size_t)b % c->rr_comm.size();
+    cudaStream_t s = k == 0 ? c->comm : c->rr_stream[k];
+    ncclComm_t comm = k == 0 ? c->nccl : c->rr_comm[k];
+    if (k) c->rr_used[k] = 1;
+    prof_begin(c, 0, s);
+    CUDA_TRY(c, launch_pack(c->dtype, sv, buf, scale, (int)c->pack_ctas, s));
+    prof_end(c, s);
+    prof_begin(c, 1, s);
     NCCL_TRY(c, ncclAllReduce(buf, buf, (size_t)bk.numel, c->dtype == DDP_FP32 ? ncclFloat32 : ncclBfloat16,
-                              ncclSum, c->nccl, c->comm));
-    prof_end(c);
-    prof_begin(c, 2);
-    CUDA_TRY(c, launch_unpack(c->dtype, sv, buf, (int)c->pack_ctas, c->comm));
-    prof_end(c);
+                              ncclSum, comm, s));
+    prof_end(c, s);
+    prof_begin(c, 2, s);
+    CUDA_TRY(c, launch_unpack(c->dtype, sv, buf, (int)c->pack_ctas, s));
+    prof_end(c, s);
     return DDP_OK;
   }
   P2PLaunch a{};
@@ -586,6 +612,7 @@ ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
     CUDA_TRY(c, cudaEventRecord(ev, s));
     CUDA_TRY(c, cudaStreamWaitEvent(c->comm, ev, 0));
     if (c->ce_pack) CUDA_TRY(c, cudaStreamWaitEvent(c->ce_pack, ev, 0));
+    for (size_t k = 1; k < c->rr_stream.size(); ++k) CUDA_TRY(c, cudaStreamWaitEvent(c->rr_stream[k], ev, 0));
     for (cudaStream_t q : c->ce_cp) CUDA_TRY(c, cudaStreamWaitEvent(q, ev, 0));
   }
   c->unwaited.clear();
@@ -621,6 +648,7 @@ void open_pass(ddp_ctx* c) {
   c->cursor = 0;
   c->n_ready = 0;
   c->trace.clear();
+  c->order.clear();
   c->un_param.clear();
   c->un_dst.clear();
   c->un_src.clear();
@@ -677,6 +705,7 @@ ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s, b
   if (c->state != State::IN_PASS) open_pass(c);
   if (c->ready[p]) return fail(DDP_ERR_DUPLICATE, "param " + std::to_string(p) + " marked ready twice");
   c->ready[p] = 1;
+  c->order.push_back(p);
   const int32_t t = c->n_ready++;
   const int32_t b = c->p_bucket[p];
   c->pending[b] -= 1;  // P:L306 pending count
@@ -720,7 +749,21 @@ const char* ddp_version(void) { return "b200ddp 0.1 (sm_100a)"; }
 
 ddp_status_t ddp_create(const int64_t* param_numel, int32_t n_params, int32_t dtype,
                         int64_t bucket_cap_bytes, int32_t world, int32_t rank, ddp_ctx_t** out) {
+  return ddp_create_ordered(param_numel, n_params, nullptr, dtype, bucket_cap_bytes, world, rank, out);
+}
+
+ddp_status_t ddp_create_ordered(const int64_t* param_numel, int32_t n_params, const int32_t* scan_order,
+                                int32_t dtype, int64_t bucket_cap_bytes, int32_t world, int32_t rank,
+                                ddp_ctx_t** out) {
   if (!out || !param_numel || n_params < 1) return fail(DDP_ERR_INVALID_ARG, "need >= 1 parameter");
+  if (scan_order) {
+    std::vector<uint8_t> seen(n_params, 0);
+    for (int32_t i = 0; i < n_params; ++i) {
+      const int32_t p = scan_order[i];
+      if (p < 0 || p >= n_params || seen[p]) return fail(DDP_ERR_INVALID_ARG, "scan_order is not a permutation");
+      seen[p] = 1;
+    }
+  }
   if (dtype != DDP_FP32 && dtype != DDP_BF16) return fail(DDP_ERR_INVALID_ARG, "dtype must be FP32 or BF16");
   if (bucket_cap_bytes < 0) return fail(DDP_ERR_INVALID_ARG, "bucket_cap_bytes < 0");
   if (world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
@@ -736,6 +779,8 @@ ddp_status_t ddp_create(const int64_t* param_numel, int32_t n_params, int32_t dt
     c->esize = dtype == DDP_FP32 ? 4 : 2;
     c->cap = bucket_cap_bytes;
     c->numel.assign(param_numel, param_numel + n_params);
+    c->scan.resize(n_params);
+    for (int32_t i = 0; i < n_params; ++i) c->scan[i] = scan_order ? scan_order[i] : n_params - 1 - i;
     assign(c);
     c->ready.assign(n_params, 0);
     c->used_local.assign(n_params, 0);
@@ -753,6 +798,15 @@ void ddp_destroy(ddp_ctx_t* c) {
   if (!c) return;
   if (c->bound && !c->emulated) {
     if (!c->poisoned && c->comm) cudaStreamSynchronize(c->comm);
+    for (size_t k = 1; k < c->rr_comm.size(); ++k) {
+      if (c->rr_stream[k] && !c->poisoned) cudaStreamSynchronize(c->rr_stream[k]);
+      if (c->rr_comm[k]) {
+        if (c->poisoned) ncclCommAbort(c->rr_comm[k]);
+        else ncclCommDestroy(c->rr_comm[k]);
+      }
+      if (c->rr_stream[k]) cudaStreamDestroy(c->rr_stream[k]);
+      if (c->rr_done[k]) cudaEventDestroy(c->rr_done[k]);
+    }
     if (c->nccl) {
       if (c->poisoned) ncclCommAbort(c->nccl);
       else ncclCommDestroy(c->nccl);
@@ -870,11 +924,26 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, 128);
   NCCL_TRY(c, ncclCommInitRank(&c->nccl, c->world, id, c->rank));
+  if (c->nccl_comms > 1) {  // round-robin groups: split k-1 more communicators off the first
+    int lo = 0, hi = 0;
+    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    c->rr_comm.assign((size_t)c->nccl_comms, nullptr);
+    c->rr_stream.assign((size_t)c->nccl_comms, nullptr);
+    c->rr_done.assign((size_t)c->nccl_comms, nullptr);
+    c->rr_used.assign((size_t)c->nccl_comms, 0);
+    c->rr_comm[0] = c->nccl;
+    c->rr_stream[0] = c->comm;
+    for (size_t k = 1; k < c->rr_comm.size(); ++k) {
+      NCCL_TRY(c, ncclCommSplit(c->nccl, 0, c->rank, &c->rr_comm[k], nullptr));
+      CUDA_TRY(c, cudaStreamCreateWithPriority(&c->rr_stream[k], cudaStreamNonBlocking, hi));
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->rr_done[k], cudaEventDisableTiming));
+    }
+  }
   char* mine = static_cast<char*>(c->storage[c->rank]);
   CUDA_TRY(c, cudaMemsetAsync(mine + c->flags_off, 0, kFlagsBytes, c->comm));
   CUDA_TRY(c, cudaMemsetAsync(mine + c->ce_flags_off, 0, (size_t)c->buckets.size() * kMaxWorld * 2 * 4, c->comm));
   bool any_ce = false;
-  for (const Bucket& bk : c->buckets) any_ce |= bk.algo == DDP_ALGO_CE;
+  for (const Bucket& bk : c->buckets) any_ce |= bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH;
   if (any_ce) {
     int lo = 0, hi = 0;
     CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -917,7 +986,7 @@ ddp_status_t ddp_bind_emulated(ddp_ctx_t* c, int32_t device, void* comm_stream, 
       return fail(DDP_ERR_INVALID_ARG, "storages must be non-null and 256-B aligned");
   }
   for (const Bucket& bk : c->buckets)
-    if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE)
+    if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH)
       return fail(DDP_ERR_UNSUPPORTED, "emulation runs the one-shot / two-shot kernels only (set DDP_OPT_ALGO)");
   if (c->find_unused) return fail(DDP_ERR_UNSUPPORTED, "find_unused needs a real communicator (no emulation)");
   if (c->multicast) return fail(DDP_ERR_UNSUPPORTED, "NVLS needs real multicast memory (no emulation)");
@@ -992,6 +1061,21 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
     const int32_t b0 = c->cursor;  // OVERLAP=0: all launches at finalize, in order
     c->cursor = nb;
     if (ddp_status_t st = launch_range(c, b0, nb, c->n_ready)) return st;
+    if (!c->dry_run) {
+      // join the side streams (copy-engine reductions and round-robin NCCL buckets
+      // write .grad / scratch there) into the comm stream: one event then covers all
+      if (c->ce_used) {
+        CUDA_TRY(c, cudaEventRecord(c->ce_red_done, c->ce_red));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_red_done, 0));
+        c->ce_used = false;
+      }
+      for (size_t k = 1; k < c->rr_stream.size(); ++k) {
+        if (!c->rr_used[k]) continue;
+        CUDA_TRY(c, cudaEventRecord(c->rr_done[k], c->rr_stream[k]));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->rr_done[k], 0));
+        c->rr_used[k] = 0;
+      }
+    }
     if (c->find_unused) {
       if (!c->dry_run) {
         if (ddp_status_t st = finish_unused(c)) return st;
@@ -1001,17 +1085,13 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
     }
     if (!c->dry_run) {
       CUDA_TRY(c, cudaEventRecord(c->comm_done, c->comm));
-      if (c->ce_used) {  // copy-engine reductions write .grad on the reduce stream
-        CUDA_TRY(c, cudaEventRecord(c->ce_red_done, c->ce_red));
-        CUDA_TRY(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), c->ce_red_done, 0));
-        c->ce_used = false;
-      }
       CUDA_TRY(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), c->comm_done, 0));
     }
   }
   c->unwaited.clear();
   for (Bucket& bk : c->buckets) std::fill(bk.grads.begin(), bk.grads.end(), nullptr);
   c->last_trace = c->trace;
+  c->last_order = c->order;
   c->state = State::IDLE;  // pending counts are replenished at the next pass open
   return DDP_OK;
 }
@@ -1052,7 +1132,7 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       c->twoshot_max = v;
       break;
     case DDP_OPT_ALGO:
-      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_NVLS) return fail(DDP_ERR_INVALID_ARG, "bad algo");
+      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_PUSH) return fail(DDP_ERR_INVALID_ARG, "bad algo");
       c->algo = v;
       break;
     case DDP_OPT_FIND_UNUSED:
@@ -1061,6 +1141,11 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
     case DDP_OPT_MULTICAST:
       c->multicast = v ? 1 : 0;
       break;
+    case DDP_OPT_NCCL_COMMS:
+      if (c->bound) return fail(DDP_ERR_STATE, "NCCL_COMMS is fixed once bound");
+      if (v < 1 || v > 8) return fail(DDP_ERR_INVALID_ARG, "NCCL_COMMS must be in [1, 8]");
+      c->nccl_comms = v;
+      return DDP_OK;
     case DDP_OPT_CE_STREAMS:
       if (c->bound) return fail(DDP_ERR_STATE, "CE_STREAMS is fixed once bound");
       if (v < 1 || v > 16) return fail(DDP_ERR_INVALID_ARG, "CE_STREAMS must be in [1, 16]");
@@ -1103,6 +1188,7 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_FIND_UNUSED: *v = c->find_unused; break;
     case DDP_OPT_MULTICAST: *v = c->multicast; break;
     case DDP_OPT_CE_STREAMS: *v = c->ce_streams; break;
+    case DDP_OPT_NCCL_COMMS: *v = c->nccl_comms; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;
@@ -1116,6 +1202,36 @@ ddp_status_t ddp_launch_trace(const ddp_ctx_t* c, int32_t* buckets, int32_t* tri
     if (buckets) buckets[i] = t[i].first;
     if (triggers) triggers[i] = t[i].second;
   }
+  return DDP_OK;
+}
+
+ddp_status_t ddp_ready_order(const ddp_ctx_t* c, int32_t* out, int32_t cap, int32_t* n) {
+  if (!c || !n || cap < 0) return fail(DDP_ERR_INVALID_ARG, "bad argument");
+  const auto& o = c->state == State::IN_PASS ? c->order : c->last_order;
+  *n = (int32_t)o.size();
+  for (int32_t i = 0; i < cap && i < (int32_t)o.size(); ++i)
+    if (out) out[i] = o[i];
+  return DDP_OK;
+}
+
+ddp_status_t ddp_broadcast(ddp_ctx_t* c, void* const* bufs, const int64_t* bytes, int32_t n, int32_t root,
+                           void* stream) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (!c->bound || c->emulated || !c->nccl) return fail(DDP_ERR_STATE, "ddp_broadcast needs a bound communicator");
+  if (c->state == State::IN_PASS) return fail(DDP_ERR_STATE, "ddp_broadcast inside a backward pass");
+  if (n < 0 || (n > 0 && (!bufs || !bytes)) || root < 0 || root >= c->world)
+    return fail(DDP_ERR_INVALID_ARG, "bad broadcast arguments");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  NCCL_TRY(c, ncclGroupStart());
+  for (int32_t i = 0; i < n; ++i) {
+    if (bytes[i] < 0 || (bytes[i] > 0 && !bufs[i])) {
+      ncclGroupEnd();
+      return fail(DDP_ERR_INVALID_ARG, "bad broadcast buffer");
+    }
+    if (bytes[i] == 0) continue;
+    NCCL_TRY(c, ncclBroadcast(bufs[i], bufs[i], (size_t)bytes[i], ncclUint8, root, c->nccl, s));
+  }
+  NCCL_TRY(c, ncclGroupEnd());
   return DDP_OK;
 }
 

@@ -74,6 +74,9 @@ struct CeView {
 };
 // own_slot[wire_k + i] = grad_k[i] (raw) for the listed (small) gradients.
 cudaError_t launch_ce_gather(int dtype, const CeView& v, void* own_slot, int max_ctas, cudaStream_t s);
+// SM push: every listed gradient (raw) to peer_slots[j] + wire_k, j < npeers.
+cudaError_t launch_ce_push(int dtype, const CeView& v, void* const* peer_slots, int npeers, int max_ctas,
+                           cudaStream_t s);
 // grad_k[i] = RNE( sum_q RNE(v_q * scale) ), rank order; v_rank = grad_k[i],
 // v_q = slot q (slot0 + q * stride_bytes) at wire_k + i.
 cudaError_t launch_ce_reduce(int dtype, int world, int rank, const CeView& v, const void* slot0,

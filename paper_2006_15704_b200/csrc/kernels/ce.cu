@@ -82,6 +82,33 @@ __global__ void __launch_bounds__(kThreads) ce_reduce_kernel(const __grid_consta
   }
 }
 
+// SM push (DDP_ALGO_PUSH): one read of every gradient, NP remote stores (the
+// same wire offset in slot `rank` of each peer).  No waiting inside the kernel:
+// the ready flags are stream memory operations after it completes.
+struct PeerDst {
+  char* p[kMaxWorld];
+};
+
+template <typename T, int NP, int MAXS>
+__global__ void __launch_bounds__(kThreads) ce_push_kernel(const __grid_constant__ CeArgs<MAXS> a,
+                                                           const __grid_constant__ PeerDst pd) {
+  constexpr int64_t tile = kTileBytes / sizeof(T);
+  const int64_t total = a.vo[a.n];
+  for (int64_t t = (int64_t)blockIdx.x * tile; t < total; t += (int64_t)gridDim.x * tile) {
+    const int64_t hi = min(t + tile, total);
+    for (int k = find_v(a, t); k < a.n && a.vo[k] < hi; ++k) {
+      const int64_t x0 = max(t, a.vo[k]), x1 = min(hi, a.vo[k + 1]);
+      if (x0 >= x1) continue;
+      const int64_t i0 = x0 - a.vo[k];
+      T* d[NP];
+#pragma unroll
+      for (int j = 0; j < NP; ++j) d[j] = reinterpret_cast<T*>(pd.p[j]) + a.wire[k] + i0;
+      const T* s[1] = {static_cast<const T*>(a.grad[k]) + i0};
+      cta_xfer<T, 1, NP, true, false>(d, s, x1 - x0, 1.0f);
+    }
+  }
+}
+
 template <int MAXS>
 CeArgs<MAXS> make_args(const CeView& v, int first, int n) {
   CeArgs<MAXS> a;
@@ -160,7 +187,49 @@ cudaError_t gather(const CeView& v, void* own_slot, int max_ctas, cudaStream_t s
   return cudaSuccess;
 }
 
+template <typename T, int NP, int MAXS>
+cudaError_t run_push(const CeView& v, int first, int n, const PeerDst& pd, int max_ctas, cudaStream_t st) {
+  const CeArgs<MAXS> a = make_args<MAXS>(v, first, n);
+  const int grid = grid_for(a.vo[n], kTileBytes / sizeof(T), max_ctas);
+  ce_push_kernel<T, NP, MAXS><<<grid, kThreads, 0, st>>>(a, pd);
+  return cudaGetLastError();
+}
+
+template <typename T, int NP>
+cudaError_t push_by_slots(const CeView& v, const PeerDst& pd, int max_ctas, cudaStream_t st) {
+  for (int first = 0; first < v.n; first += kMaxSlotsPerLaunch) {
+    const int n = v.n - first < kMaxSlotsPerLaunch ? v.n - first : kMaxSlotsPerLaunch;
+    cudaError_t e = n <= 32    ? run_push<T, NP, 32>(v, first, n, pd, max_ctas, st)
+                    : n <= 256 ? run_push<T, NP, 256>(v, first, n, pd, max_ctas, st)
+                               : run_push<T, NP, 1024>(v, first, n, pd, max_ctas, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+template <typename T>
+cudaError_t push_by_world(int npeers, const CeView& v, const PeerDst& pd, int max_ctas, cudaStream_t st) {
+  switch (npeers) {
+    case 1: return push_by_slots<T, 1>(v, pd, max_ctas, st);
+    case 2: return push_by_slots<T, 2>(v, pd, max_ctas, st);
+    case 3: return push_by_slots<T, 3>(v, pd, max_ctas, st);
+    case 4: return push_by_slots<T, 4>(v, pd, max_ctas, st);
+    case 5: return push_by_slots<T, 5>(v, pd, max_ctas, st);
+    case 6: return push_by_slots<T, 6>(v, pd, max_ctas, st);
+    case 7: return push_by_slots<T, 7>(v, pd, max_ctas, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_ce_push(int dtype, const CeView& v, void* const* peer_slots, int npeers, int max_ctas,
+                           cudaStream_t s) {
+  PeerDst pd{};
+  for (int j = 0; j < npeers && j < kMaxWorld; ++j) pd.p[j] = static_cast<char*>(peer_slots[j]);
+  return dtype == 0 ? push_by_world<float>(npeers, v, pd, max_ctas, s)
+                    : push_by_world<__nv_bfloat16>(npeers, v, pd, max_ctas, s);
+}
 
 cudaError_t launch_ce_gather(int dtype, const CeView& v, void* own_slot, int max_ctas, cudaStream_t s) {
   if (v.n == 0) return cudaSuccess;

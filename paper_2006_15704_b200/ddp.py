@@ -53,13 +53,14 @@ class GradReducer:
 
     def __init__(self, numels: Sequence[int], dtype="fp32", bucket_cap_bytes: int = 25 * MIB,
                  group=None, device: Optional[torch.device] = None,
-                 options: Optional[Dict[int, int]] = None, comm_stream: Optional[torch.cuda.Stream] = None):
+                 options: Optional[Dict[int, int]] = None, comm_stream: Optional[torch.cuda.Stream] = None,
+                 scan_order: Optional[Sequence[int]] = None):
         self.rank, self.world = _group_info(group)
         self.group = group
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.numels = [int(n) for n in numels]
         self.dtype = _DTYPES[dtype]
-        self.ctx = L.ddp_create(self.numels, self.dtype, bucket_cap_bytes, self.world, self.rank)
+        self.ctx = L.ddp_create_ordered(self.numels, scan_order, self.dtype, bucket_cap_bytes, self.world, self.rank)
         try:
             for k, v in (options or {}).items():
                 L.ddp_set_option(self.ctx, k, v)
@@ -131,6 +132,16 @@ class GradReducer:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         L.ddp_mark_unused(self.ctx, param_idx, 0 if grad is None else grad.data_ptr(), s.cuda_stream)
 
+    def ready_order(self) -> List[int]:
+        return L.ddp_ready_order(self.ctx)
+
+    def broadcast(self, tensors: Sequence[torch.Tensor], root: int = 0,
+                  stream: Optional[torch.cuda.Stream] = None):
+        """In-place broadcast of contiguous device tensors from `root` (one NCCL group)."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        L.ddp_broadcast(self.ctx, [t.data_ptr() for t in tensors],
+                        [t.numel() * t.element_size() for t in tensors], root, s.cuda_stream)
+
     def global_unused(self) -> List[bool]:
         return L.ddp_global_unused(self.ctx, len(self.numels))
 
@@ -189,15 +200,23 @@ class DistributedDataParallel(torch.nn.Module):
 
     Constructor: ``process_group``, ``bucket_cap_mb``
     (default 25, read as MiB, C-5).  ``broadcast_parameters``: rank 0's
-    parameters are copied to every rank at construction (Alg. 1),
-    via torch's broadcast (plumbing, not the hot path).
+    parameters (and buffers) are copied to every rank at construction (Alg. 1
+    L214-L215) through the library's communicator (``ddp_broadcast``).
+    ``find_unused_parameters``: Alg. 1 forward L224-L225.
+    ``rebuild_buckets``: gradient order prediction — after the
+    first synced backward, rank 0's traced ready order is broadcast and the
+    parameter-to-bucket map is rebuilt from it once, at the next forward.
     """
 
     def __init__(self, module: torch.nn.Module, process_group=None, bucket_cap_mb: float = 25,
                  broadcast_parameters: bool = True, options: Optional[Dict[int, int]] = None,
-                 find_unused_parameters: bool = False):
+                 find_unused_parameters: bool = False, rebuild_buckets: bool = False):
         super().__init__()
         self.find_unused_parameters = find_unused_parameters
+        self.process_group = process_group
+        self.bucket_cap_mb = bucket_cap_mb
+        self._rebuild = rebuild_buckets
+        self._new_order: Optional[List[int]] = None
         options = dict(options or {})
         if find_unused_parameters:
             options[L.OPT_FIND_UNUSED] = 1
@@ -206,13 +225,15 @@ class DistributedDataParallel(torch.nn.Module):
         dtypes = {p.dtype for p in self.params}
         if len(dtypes) != 1:
             raise ValueError("one gradient dtype per reducer (reading C-11)")
-        if broadcast_parameters and dist.is_available() and dist.is_initialized():
-            with torch.no_grad():
-                for p in self.params:
-                    dist.broadcast(p.data, src=0, group=process_group)
-        self.reducer = GradReducer([p.numel() for p in self.params], dtypes.pop(),
+        self._dtype = dtypes.pop()
+        self._options = options
+        self.reducer = GradReducer([p.numel() for p in self.params], self._dtype,
                                    int(bucket_cap_mb * MIB), group=process_group,
                                    device=self.params[0].device, options=options)
+        if broadcast_parameters and self.reducer.world > 1:
+            states = [t for t in list(module.parameters()) + list(module.buffers()) if t.is_contiguous()]
+            with torch.no_grad():
+                self.reducer.broadcast([t.data for t in states], root=0)
         self._pass_open = False
         self._in_no_sync = False
         self._unused_bufs: Dict[int, torch.Tensor] = {}
@@ -235,6 +256,13 @@ class DistributedDataParallel(torch.nn.Module):
     def _finalize(self):
         self._pass_open = False
         self.reducer.finalize()
+        if self._rebuild and not self._in_no_sync:
+            self._rebuild = False
+            order = torch.tensor(self.reducer.ready_order(), dtype=torch.int32, device=self.params[0].device)
+            if self.reducer.world > 1:
+                dist.broadcast(order, src=dist.get_global_rank(self.process_group, 0)
+                               if self.process_group is not None else 0, group=self.process_group)
+            self._new_order = order.tolist()
         if self._unused_bufs:
             # locally-unused params without a .grad got a zero buffer as their
             # destination; attach it only where some rank used the param (the
@@ -245,7 +273,18 @@ class DistributedDataParallel(torch.nn.Module):
                     self.params[i].grad = buf
             self._unused_bufs = {}
 
+    def _rebuild_reducer(self):
+        """Rebuild the parameter-to-bucket map from the agreed traced order (rare;
+        re-allocates the symmetric storage, a collective)."""
+        order, self._new_order = self._new_order, None
+        self.reducer.close()
+        self.reducer = GradReducer([p.numel() for p in self.params], self._dtype,
+                                   int(self.bucket_cap_mb * MIB), group=self.process_group,
+                                   device=self.params[0].device, options=self._options, scan_order=order)
+
     def forward(self, *args, **kwargs):
+        if self._new_order is not None:
+            self._rebuild_reducer()
         out = self.module(*args, **kwargs)
         if self.find_unused_parameters and torch.is_grad_enabled():
             self._mark_unused(out)

@@ -299,3 +299,64 @@ def test_mark_unused_accumulated_grad_required():
         L.ddp_finalize_backward(ctx, 0)
     finally:
         L.ddp_destroy(ctx)
+
+
+def test_create_ordered_mapping_vs_oracle():
+    """ddp_create_ordered (gradient order prediction): the map built
+    from an explicit scan order equals the oracle's, bit-exactly; the reverse
+    registration order reproduces ddp_create; non-permutations are rejected."""
+    rng = random.Random(11)
+    for model, cap in [("toy", 4096), ("resnet50", 5 * MIB), ("bert_large", 25 * MIB)]:
+        ns = numels(model)
+        order = list(range(len(ns)))
+        rng.shuffle(order)
+        ctx = L.ddp_create_ordered(ns, order, L.FP32, cap, 1, 0)
+        try:
+            assert _mapping(ctx) == _oracle_mapping(assign_buckets(ns, 4, cap, order))
+        finally:
+            L.ddp_destroy(ctx)
+        rev = list(range(len(ns) - 1, -1, -1))
+        c1, c2 = L.ddp_create_ordered(ns, rev, L.FP32, cap, 1, 0), L.ddp_create(ns, L.FP32, cap, 1, 0)
+        try:
+            assert _mapping(c1) == _mapping(c2)
+        finally:
+            L.ddp_destroy(c1)
+            L.ddp_destroy(c2)
+    for bad in ([0, 0, 1, 2, 3, 4], [0, 1, 2, 3, 4, 6], [0, 1, 2]):
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_create_ordered(numels("toy"), bad + [0] * (6 - len(bad)) if len(bad) < 6 else bad,
+                                 L.FP32, 4096, 1, 0)
+        assert e.value.status == L.ERR_INVALID_ARG
+
+
+def test_rebuild_from_traced_order_launches_without_deferral():
+    """Trace a pass whose hooks fire in a non-reverse order (ddp_ready_order),
+    rebuild the map from it: every bucket then launches exactly at the signal
+    of its last slot — no bucket waits behind an earlier one (P:L197 caveat),
+    which the replay oracle O-2 confirms."""
+    ns = numels("resnet50")
+    rng = random.Random(5)
+    order = list(range(len(ns)))
+    rng.shuffle(order)
+    ctx = L.ddp_create(ns, L.FP32, 5 * MIB, 1, 0)
+    try:
+        L.ddp_set_option(ctx, L.OPT_DRY_RUN, 1)
+        for p in order:
+            L.ddp_grad_ready(ctx, p, 0, 0)
+        L.ddp_finalize_backward(ctx, 0)
+        assert L.ddp_ready_order(ctx) == order
+    finally:
+        L.ddp_destroy(ctx)
+    ctx = L.ddp_create_ordered(ns, order, L.FP32, 5 * MIB, 1, 0)
+    try:
+        L.ddp_set_option(ctx, L.OPT_DRY_RUN, 1)
+        for p in order:
+            L.ddp_grad_ready(ctx, p, 0, 0)
+        L.ddp_finalize_backward(ctx, 0)
+        tr = L.ddp_launch_trace(ctx)
+        a = assign_buckets(ns, 4, 5 * MIB, order)
+        assert tr == replay(a, order)
+        ends = list(itertools.accumulate(len(s) for s in a.buckets))
+        assert [t for _, t in tr] == [e - 1 for e in ends]
+    finally:
+        L.ddp_destroy(ctx)

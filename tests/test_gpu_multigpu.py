@@ -47,9 +47,10 @@ def _worker(rank, world, init_file, cfgs, q):
     from tests.gpu_util import TDT, to_np
     out = []
     try:
-        for (model, dtype, cap, algo, iters) in cfgs:
+        for cfg in cfgs:
+            model, dtype, cap, algo, iters = cfg[:5]
             ns = numels(model)
-            red = GradReducer(ns, dtype, cap, options={L.OPT_ALGO: algo})
+            red = GradReducer(ns, dtype, cap, options={L.OPT_ALGO: algo, **(cfg[5] if len(cfg) > 5 else {})})
             grads = [torch.empty(n, dtype=TDT[dtype], device="cuda") for n in ns]
             idx = [torch.from_numpy(_sample_idx(p, n)).cuda() for p, n in enumerate(ns)]
             res = []
@@ -103,9 +104,14 @@ def test_multigpu_parity(world):
             ("toy", "bf16", 4096, L.ALGO_CE, 3), ("resnet50", "fp32", 25 * MIB, L.ALGO_CE, 2),
             ("bert_large", "bf16", 25 * MIB, L.ALGO_CE, 1),
             ("toy", "fp32", 4096, L.ALGO_NVLS, 2), ("resnet50", "bf16", 25 * MIB, L.ALGO_NVLS, 1),
-            ("resnet50", "fp32", 5 * MIB, L.ALGO_NVLS, 1)]
+            ("resnet50", "fp32", 5 * MIB, L.ALGO_NVLS, 1),
+            ("resnet50", "fp32", 5 * MIB, L.ALGO_NCCL, 2, {L.OPT_NCCL_COMMS: 3}),   # round-robin groups
+            ("resnet50", "bf16", 5 * MIB, L.ALGO_CE, 2, {L.OPT_CE_STREAMS: 1}),
+            ("toy", "fp32", 4096, L.ALGO_PUSH, 3), ("resnet50", "bf16", 25 * MIB, L.ALGO_PUSH, 2),
+            ("bert_large", "fp32", 25 * MIB, L.ALGO_PUSH, 1)]
     outs = _run(world, cfgs)
-    for ci, (model, dtype, cap, algo, iters) in enumerate(cfgs):
+    for ci, cfg in enumerate(cfgs):
+        model, dtype, cap, algo, iters = cfg[:5]
         ns = numels(model)
         algos = outs[0][ci][1]
         tol = any(x in ("nccl", "nvls") for x in algos)   # not rank-order sums: tolerance parity

@@ -123,3 +123,36 @@ def test_invalid_args():
             assign_buckets(bad, 4, 10)
     with pytest.raises(ValueError):
         assign_buckets([3], 4, -1)
+
+
+def _brute_force_order(ns, esize, cap, order):
+    """Longest-prefix formulation over an explicit scan order."""
+    rest, out = list(order), []
+    while rest:
+        best = 1
+        for k in range(1, len(rest) + 1):
+            if sum(ns[p] for p in rest[:k]) * esize <= cap:
+                best = k
+        out.append(rest[:best])
+        rest = rest[best:]
+    return out
+
+
+def test_explicit_order_brute_force_and_invariants():
+    """O-1 with a traced scan order: same greedy rule, scan order
+    preserved along the buckets; reverse registration order = the default."""
+    rng = random.Random(563)
+    for _ in range(300):
+        n = rng.randint(1, 9)
+        ns = [rng.randint(1, 50) for _ in range(n)]
+        esize = rng.choice([1, 2, 4])
+        cap = rng.choice([0, rng.randint(1, 300), 10 ** 9])
+        order = list(range(n))
+        rng.shuffle(order)
+        a = assign_buckets(ns, esize, cap, order)
+        assert _params_per_bucket(a) == _brute_force_order(ns, esize, cap, order)
+        assert [p for slots in a.buckets for p, _ in slots] == order
+        d = assign_buckets(ns, esize, cap, list(range(n - 1, -1, -1)))
+        assert _params_per_bucket(d) == _params_per_bucket(assign_buckets(ns, esize, cap))
+    with pytest.raises(ValueError):
+        assign_buckets([1, 2, 3], 4, 10, [0, 0, 1])
