@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--pack-ctas", type=int, default=0)
     ap.add_argument("--stage-kib", type=int, default=0)
     ap.add_argument("--ce-streams", type=int, default=0)
+    ap.add_argument("--ce-direct-mib", type=float, default=-1, help="CE: copy gradients >= this straight from .grad")
     ap.add_argument("--nccl-comms", type=int, default=0, help="round-robin NCCL communicators (P:L535)")
     ap.add_argument("--exposed-model", default="resnet50", choices=["none", "resnet50", "bert_large"],
                     help="real-model backward for the exposed-time measurement")
@@ -219,6 +220,8 @@ def run_ours(a):
         opts[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
     if a.ce_streams:
         opts[L.OPT_CE_STREAMS] = a.ce_streams
+    if a.ce_direct_mib >= 0:
+        opts[L.OPT_CE_DIRECT_BYTES] = int(a.ce_direct_mib * MIB)
     if a.nccl_comms:
         opts[L.OPT_NCCL_COMMS] = a.nccl_comms
     if a.oneshot_max >= 0:
@@ -303,12 +306,12 @@ def run_ours(a):
     peak_hbm, peak_src = measured_peaks()
     kinds = {k: v for k, v in prof.items() if v[1] > 0}
     dom = max(kinds, key=lambda k: kinds[k][0]) if kinds else None
-    small = 0   # CE buckets: bytes of the gradients gathered by the pack kernel (< 1 MiB each)
+    small = 0   # CE buckets: bytes of the gradients gathered by the pack kernel (< CE_DIRECT_BYTES each)
     for b, x in enumerate(algos):
         if x == "ce":
             for s_ in range(L.ddp_bucket_info(red.ctx, b)[1]):
                 p, _ = L.ddp_bucket_slot(red.ctx, b, s_)
-                small += ns[p] * esize if ns[p] * esize < (1 << 20) else 0
+                small += ns[p] * esize if ns[p] * esize < L.ddp_get_option(red.ctx, L.OPT_CE_DIRECT_BYTES) else 0
     by = {x: sum(n * esize for n, y in zip(bnumel, algos) if y == x) for x in ("nccl", "oneshot", "twoshot", "ce", "nvls", "push")}
 
     def kind_bytes(kind):
@@ -626,6 +629,8 @@ def _opts(a):
         o[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
     if a.ce_streams:
         o[L.OPT_CE_STREAMS] = a.ce_streams
+    if a.ce_direct_mib >= 0:
+        o[L.OPT_CE_DIRECT_BYTES] = int(a.ce_direct_mib * MIB)
     if a.nccl_comms:
         o[L.OPT_NCCL_COMMS] = a.nccl_comms
     if a.oneshot_max >= 0:

@@ -88,9 +88,12 @@ enum {
                                    rank must agree.  Never increases ddp_storage_bytes */
   DDP_OPT_CE_STREAMS = 12,      /* copy-engine algorithm: number of streams its peer copies are
                                    spread over (1..16, default 4); before binding only */
-  DDP_OPT_NCCL_COMMS = 13       /* round-robin process groups (Fig. 12 "rrx"): NCCL
+  DDP_OPT_NCCL_COMMS = 13,      /* round-robin process groups (Fig. 12 "rrx"): NCCL
                                    bucket b runs on communicator b mod k (split off the first with
                                    ncclCommSplit) and its own stream; 1..8, default 1; before binding */
+  DDP_OPT_CE_DIRECT_BYTES = 14  /* CE algorithm: gradients >= this many bytes are copied straight
+                                   from .grad (one copy per peer); smaller ones are gathered into
+                                   one region first.  Default 16 MiB; layout key */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.

@@ -45,10 +45,6 @@ constexpr int64_t kMinChunkElems = 4096;   // smallest per-CTA chunk worth a CTA
 // stage per chunk (one sync for one-shot, two for two-shot); DDP_OPT_P2P_STAGE_BYTES
 // splits chunks for experiments.
 constexpr int64_t kBarrierScratch = 32 * 1024;  // scratch int inside the flags region
-// Copy-engine algorithm: gradients of at least this many bytes travel straight
-// from .grad (one cudaMemcpyAsync per peer); smaller ones are gathered into one
-// region first (a copy-engine transfer costs a few us of fixed latency).
-constexpr int64_t kCeDirectBytes = 1 << 20;
 constexpr int64_t kCeWireAlign = 64;  // elements: wire offsets keep 16-B (and 256-B) alignment
 
 struct Bucket {
@@ -93,7 +89,11 @@ struct ddp_ctx {
   // NVLink bytes as two-shot with one sync instead of two; world > 2: <= 512 KiB)
   int64_t overlap = 1, oneshot_max = -1, twoshot_max = INT64_MAX, comm_ctas = 64,
           dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 8, stage_bytes = 0,
-          find_unused = 0, multicast = 0, ce_streams = 4, nccl_comms = 1;
+          find_unused = 0, multicast = 0, ce_streams = 4, nccl_comms = 1,
+          // CE: gradients of at least this many bytes travel straight from .grad (one
+          // cudaMemcpyAsync per peer, a few us of host + copy-engine fixed cost each);
+          // smaller ones are gathered into one region first (2x their bytes of HBM)
+          ce_direct = 16 << 20;
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
           stage1_stride = 0, ce_flags_off = 0, bitmap_off = 0, scratch_off = 0, storage_bytes = 0;
@@ -297,7 +297,7 @@ void plan(ddp_ctx* c) {
       if (pass == 1) bk.ce_small0 = w;
       for (size_t k = 0; k < ns; ++k) {
         const int64_t n = bk.off[k + 1] - bk.off[k];
-        const bool direct = bk.algo == DDP_ALGO_CE && n * c->esize >= kCeDirectBytes;
+        const bool direct = bk.algo == DDP_ALGO_CE && n * c->esize >= c->ce_direct;
         if (direct != (pass == 0)) continue;
         bk.ce_direct[k] = direct;
         bk.ce_wire[k] = w;
@@ -736,7 +736,7 @@ ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s, b
 
 bool is_layout_key(int32_t k) {
   return k == DDP_OPT_P2P_ONESHOT_MAX || k == DDP_OPT_P2P_TWOSHOT_MAX || k == DDP_OPT_ALGO ||
-         k == DDP_OPT_FIND_UNUSED || k == DDP_OPT_MULTICAST;
+         k == DDP_OPT_FIND_UNUSED || k == DDP_OPT_MULTICAST || k == DDP_OPT_CE_DIRECT_BYTES;
 }
 
 }  // namespace
@@ -1141,6 +1141,10 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
     case DDP_OPT_MULTICAST:
       c->multicast = v ? 1 : 0;
       break;
+    case DDP_OPT_CE_DIRECT_BYTES:
+      if (v < 0) return fail(DDP_ERR_INVALID_ARG, "negative CE_DIRECT_BYTES");
+      c->ce_direct = v;
+      break;
     case DDP_OPT_NCCL_COMMS:
       if (c->bound) return fail(DDP_ERR_STATE, "NCCL_COMMS is fixed once bound");
       if (v < 1 || v > 8) return fail(DDP_ERR_INVALID_ARG, "NCCL_COMMS must be in [1, 8]");
@@ -1189,6 +1193,7 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_MULTICAST: *v = c->multicast; break;
     case DDP_OPT_CE_STREAMS: *v = c->ce_streams; break;
     case DDP_OPT_NCCL_COMMS: *v = c->nccl_comms; break;
+    case DDP_OPT_CE_DIRECT_BYTES: *v = c->ce_direct; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;
