@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--pack-ctas", type=int, default=0)
     ap.add_argument("--stage-kib", type=int, default=0)
     ap.add_argument("--ce-streams", type=int, default=0)
+    ap.add_argument("--wire-bf16", action="store_true", help="N-3: fp32 gradients travel as bf16 (CE exchange)")
     ap.add_argument("--ce-direct-mib", type=float, default=-1, help="CE: copy gradients >= this straight from .grad")
     ap.add_argument("--nccl-comms", type=int, default=0, help="round-robin NCCL communicators (P:L535)")
     ap.add_argument("--exposed-model", default="resnet50", choices=["none", "resnet50", "bert_large"],
@@ -220,6 +221,8 @@ def run_ours(a):
         opts[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
     if a.ce_streams:
         opts[L.OPT_CE_STREAMS] = a.ce_streams
+    if a.wire_bf16:
+        opts[L.OPT_WIRE_BF16] = 1
     if a.ce_direct_mib >= 0:
         opts[L.OPT_CE_DIRECT_BYTES] = int(a.ce_direct_mib * MIB)
     if a.nccl_comms:
@@ -423,7 +426,7 @@ def run_ours(a):
         line = {
             "metric": METRIC, "value": ms, "unit": "ms/iter", "n_gpus": world, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32" if a.dtype == "fp32" else "bf16",
+            "vs_baseline": None, "dtype": ("f32 (bf16 wire)" if a.wire_bf16 else "f32") if a.dtype == "fp32" else "bf16",
             "data": "synthetic (seeded splitmix64 gradients shaped like the workload; no model compute)",
             "config": {"workload": workload_name(a), "params": sum(ns), "tensors": len(ns),
                        "buckets": len(bnumel), "bucket_algos": algos, "bucket_cap_mib": a.cap_mib,
@@ -629,6 +632,8 @@ def _opts(a):
         o[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
     if a.ce_streams:
         o[L.OPT_CE_STREAMS] = a.ce_streams
+    if a.wire_bf16:
+        o[L.OPT_WIRE_BF16] = 1
     if a.ce_direct_mib >= 0:
         o[L.OPT_CE_DIRECT_BYTES] = int(a.ce_direct_mib * MIB)
     if a.nccl_comms:

@@ -85,15 +85,15 @@ struct ddp_ctx {
   std::vector<int32_t> p_bucket, p_slot;
   std::vector<int64_t> p_off;
   // options
-  // oneshot_max < 0: automatic (world 2: every bucket one-shot — it sends the same
-  // NVLink bytes as two-shot with one sync instead of two; world > 2: <= 512 KiB)
+  // oneshot_max < 0: automatic (world 2: <= 1 MiB; world > 2: <= 512 KiB)
   int64_t overlap = 1, oneshot_max = -1, twoshot_max = INT64_MAX, comm_ctas = 64,
           dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 8, stage_bytes = 0,
           find_unused = 0, multicast = 0, ce_streams = 4, nccl_comms = 1,
           // CE: gradients of at least this many bytes travel straight from .grad (one
           // cudaMemcpyAsync per peer, a few us of host + copy-engine fixed cost each);
           // smaller ones are gathered into one region first (2x their bytes of HBM)
-          ce_direct = 16 << 20;
+          ce_direct = 16 << 20,
+          wire_bf16 = 0;  // N-3: fp32 gradients travel as bf16 (CE exchange)
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
           stage1_stride = 0, ce_flags_off = 0, bitmap_off = 0, scratch_off = 0, storage_bytes = 0;
@@ -219,13 +219,20 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   if (c->algo != DDP_ALGO_AUTO) {
     a = (int)c->algo;
     if (c->world == 1 && (a == DDP_ALGO_CE || a == DDP_ALGO_NVLS || a == DDP_ALGO_PUSH)) a = DDP_ALGO_ONESHOT;
+    if (c->world > 1 && c->wire_bf16) a = DDP_ALGO_CE;  // the compressed wire is a CE feature
     if (a == DDP_ALGO_NVLS && !c->multicast) a = DDP_ALGO_TWOSHOT;
   } else if (c->world == 1) {
     a = DDP_ALGO_ONESHOT;
-  } else if (bytes <= (c->oneshot_max >= 0 ? c->oneshot_max : c->world == 2 ? INT64_MAX : 512 * 1024)) {
-    a = DDP_ALGO_ONESHOT;
+  } else if (c->wire_bf16) {
+    a = DDP_ALGO_CE;
+  } else if (bytes <= (c->oneshot_max >= 0 ? c->oneshot_max : c->world == 2 ? (1 << 20) : 512 * 1024)) {
+    a = DDP_ALGO_ONESHOT;  // latency-bound: one fused kernel, one barrier
   } else if (bytes <= c->twoshot_max) {
-    a = c->multicast ? DDP_ALGO_NVLS : DDP_ALGO_TWOSHOT;
+    // world 2: the copy-engine exchange moves the same (W-1) S = S bytes as any
+    // algorithm, keeps the SMs free for backward and pipelines buckets
+    // (profiles/r01_n2.md); wider: fewer NVLink bytes win — NVLS (1+1/W) S, else
+    // two-shot 2(W-1)/W S
+    a = c->world == 2 ? DDP_ALGO_CE : c->multicast ? DDP_ALGO_NVLS : DDP_ALGO_TWOSHOT;
   } else {
     a = DDP_ALGO_NCCL;
   }
@@ -297,7 +304,7 @@ void plan(ddp_ctx* c) {
       if (pass == 1) bk.ce_small0 = w;
       for (size_t k = 0; k < ns; ++k) {
         const int64_t n = bk.off[k + 1] - bk.off[k];
-        const bool direct = bk.algo == DDP_ALGO_CE && n * c->esize >= c->ce_direct;
+        const bool direct = bk.algo == DDP_ALGO_CE && !c->wire_bf16 && n * c->esize >= c->ce_direct;
         if (direct != (pass == 0)) continue;
         bk.ce_direct[k] = direct;
         bk.ce_wire[k] = w;
@@ -305,7 +312,7 @@ void plan(ddp_ctx* c) {
       }
     }
     bk.ce_wire_numel = w;
-    bk.ce_stride = align_up(w * c->esize, 256);
+    bk.ce_stride = align_up(w * (c->wire_bf16 ? 2 : c->esize), 256);
     bk.ce_off = pos;
     pos += c->world * bk.ce_stride;
   }
@@ -400,10 +407,13 @@ ddp_status_t launch_ce(ddp_ctx* c, int b) {
     c->ce_numel.push_back(bk.off[k + 1] - bk.off[k]);
   }
   const bool any_small = !c->ce_grad.empty();
+  const int64_t we = c->wire_bf16 ? 2 : c->esize;  // wire element bytes
+  const float scale = 1.0f / (float)W;
   if (any_small) {  // gather on its own stream so it overlaps the previous bucket's copies
     const CeView gv{c->ce_grad.data(), c->ce_wire.data(), c->ce_numel.data(), (int32_t)c->ce_grad.size()};
     prof_begin(c, 0, c->ce_pack);
-    CUDA_TRY(c, launch_ce_gather(c->dtype, gv, own_slot, (int)c->pack_ctas, c->ce_pack));
+    if (c->wire_bf16) CUDA_TRY(c, launch_wire_gather(gv, own_slot, scale, (int)c->pack_ctas, c->ce_pack));
+    else CUDA_TRY(c, launch_ce_gather(c->dtype, gv, own_slot, (int)c->pack_ctas, c->ce_pack));
     prof_end(c, c->ce_pack);
     CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
     CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_packed[b], 0));
@@ -452,8 +462,8 @@ ddp_status_t launch_ce(ddp_ctx* c, int b) {
         if (ddp_status_t st = issue(dst + bk.ce_wire[k] * c->esize, bk.grads[k], (bk.off[k + 1] - bk.off[k]) * c->esize))
           return st;
     if (any_small)
-      if (ddp_status_t st = issue(dst + bk.ce_small0 * c->esize, own_slot + bk.ce_small0 * c->esize,
-                                  (bk.ce_wire_numel - bk.ce_small0) * c->esize))
+      if (ddp_status_t st = issue(dst + bk.ce_small0 * we, own_slot + bk.ce_small0 * we,
+                                  (bk.ce_wire_numel - bk.ce_small0) * we))
         return st;
   }
   for (int q = 0; q < K; ++q) {
@@ -478,8 +488,11 @@ ddp_status_t launch_ce(ddp_ctx* c, int b) {
   for (size_t k = 0; k < ns; ++k) c->ce_numel.push_back(bk.off[k + 1] - bk.off[k]);
   const CeView rv{c->ce_grad.data(), c->ce_wire.data(), c->ce_numel.data(), (int32_t)ns};
   prof_begin(c, 5, c->ce_red);
-  CUDA_TRY(c, launch_ce_reduce(c->dtype, W, r, rv, mine + bk.ce_off, bk.ce_stride, 1.0f / (float)W,
-                               (int)c->pack_ctas, c->ce_red));
+  if (c->wire_bf16)
+    CUDA_TRY(c, launch_wire_reduce(W, r, rv, mine + bk.ce_off, bk.ce_stride, scale, (int)c->pack_ctas, c->ce_red));
+  else
+    CUDA_TRY(c, launch_ce_reduce(c->dtype, W, r, rv, mine + bk.ce_off, bk.ce_stride, scale, (int)c->pack_ctas,
+                                 c->ce_red));
   prof_end(c, c->ce_red);
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
@@ -736,7 +749,8 @@ ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s, b
 
 bool is_layout_key(int32_t k) {
   return k == DDP_OPT_P2P_ONESHOT_MAX || k == DDP_OPT_P2P_TWOSHOT_MAX || k == DDP_OPT_ALGO ||
-         k == DDP_OPT_FIND_UNUSED || k == DDP_OPT_MULTICAST || k == DDP_OPT_CE_DIRECT_BYTES;
+         k == DDP_OPT_FIND_UNUSED || k == DDP_OPT_MULTICAST || k == DDP_OPT_CE_DIRECT_BYTES ||
+         k == DDP_OPT_WIRE_BF16;
 }
 
 }  // namespace
@@ -1145,6 +1159,10 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       if (v < 0) return fail(DDP_ERR_INVALID_ARG, "negative CE_DIRECT_BYTES");
       c->ce_direct = v;
       break;
+    case DDP_OPT_WIRE_BF16:
+      if (v && c->dtype != DDP_FP32) return fail(DDP_ERR_INVALID_ARG, "WIRE_BF16 compresses fp32 gradients only");
+      c->wire_bf16 = v ? 1 : 0;
+      break;
     case DDP_OPT_NCCL_COMMS:
       if (c->bound) return fail(DDP_ERR_STATE, "NCCL_COMMS is fixed once bound");
       if (v < 1 || v > 8) return fail(DDP_ERR_INVALID_ARG, "NCCL_COMMS must be in [1, 8]");
@@ -1194,6 +1212,7 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_CE_STREAMS: *v = c->ce_streams; break;
     case DDP_OPT_NCCL_COMMS: *v = c->nccl_comms; break;
     case DDP_OPT_CE_DIRECT_BYTES: *v = c->ce_direct; break;
+    case DDP_OPT_WIRE_BF16: *v = c->wire_bf16; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;

@@ -77,6 +77,11 @@ cudaError_t launch_ce_gather(int dtype, const CeView& v, void* own_slot, int max
 // SM push: every listed gradient (raw) to peer_slots[j] + wire_k, j < npeers.
 cudaError_t launch_ce_push(int dtype, const CeView& v, void* const* peer_slots, int npeers, int max_ctas,
                            cudaStream_t s);
+// Compressed wire (fp32 gradients, bf16 slots): gather converts RNE_bf16(g * scale);
+// reduce sums fp32(v_q) in rank order, v_rank recomputed from .grad, fp32 result.
+cudaError_t launch_wire_gather(const CeView& v, void* own_slot, float scale, int max_ctas, cudaStream_t s);
+cudaError_t launch_wire_reduce(int world, int rank, const CeView& v, const void* slot0, int64_t stride_bytes,
+                               float scale, int max_ctas, cudaStream_t s);
 // grad_k[i] = RNE( sum_q RNE(v_q * scale) ), rank order; v_rank = grad_k[i],
 // v_q = slot q (slot0 + q * stride_bytes) at wire_k + i.
 cudaError_t launch_ce_reduce(int dtype, int world, int rank, const CeView& v, const void* slot0,

@@ -150,21 +150,19 @@ __device__ __forceinline__ void cta_xfer(T* const (&dst)[ND], const T* const (&s
     for (int j = 0; j < ND; ++j) st_v4(dst[j] + head + v * VE, y);
   };
   auto ldv = [&](const T* p) -> uint4 { return SRC_NC ? ld_nc_v4(p) : ld_cg_v4(p); };
-  int64_t v = tid;
-  for (; v + (int64_t)(U - 1) * nt < nv; v += (int64_t)U * nt) {
+  // U vectors per source in flight per thread; the last round is predicated so a
+  // partial round still keeps its loads in flight together
+  for (int64_t v = tid; v < nv; v += (int64_t)U * nt) {
     uint4 in[U][NS];
 #pragma unroll
     for (int u = 0; u < U; ++u)
+      if (v + (int64_t)u * nt < nv) {
 #pragma unroll
-      for (int k = 0; k < NS; ++k) in[u][k] = ldv(src[k] + head + (v + (int64_t)u * nt) * VE);
+        for (int k = 0; k < NS; ++k) in[u][k] = ldv(src[k] + head + (v + (int64_t)u * nt) * VE);
+      }
 #pragma unroll
-    for (int u = 0; u < U; ++u) vec(v + (int64_t)u * nt, in[u]);
-  }
-  for (; v < nv; v += nt) {
-    uint4 in[NS];
-#pragma unroll
-    for (int k = 0; k < NS; ++k) in[k] = ldv(src[k] + head + v * VE);
-    vec(v, in);
+    for (int u = 0; u < U; ++u)
+      if (v + (int64_t)u * nt < nv) vec(v + (int64_t)u * nt, in[u]);
   }
   for (int64_t i = head + nv * VE + tid; i < n; i += nt) scalar(i);
 }

@@ -19,6 +19,7 @@ import torch.multiprocessing as mp
 
 from oracle.assignment import MIB
 from oracle.average import average_bitfaithful, average_fp64, to_fp32
+from oracle.compress import average_bf16_wire
 from synth.gen import gen_values
 from synth.shapes import numels
 
@@ -108,13 +109,16 @@ def test_multigpu_parity(world):
             ("resnet50", "fp32", 5 * MIB, L.ALGO_NCCL, 2, {L.OPT_NCCL_COMMS: 3}),   # round-robin groups
             ("resnet50", "bf16", 5 * MIB, L.ALGO_CE, 2, {L.OPT_CE_STREAMS: 1}),
             ("toy", "fp32", 4096, L.ALGO_PUSH, 3), ("resnet50", "bf16", 25 * MIB, L.ALGO_PUSH, 2),
-            ("bert_large", "fp32", 25 * MIB, L.ALGO_PUSH, 1)]
+            ("bert_large", "fp32", 25 * MIB, L.ALGO_PUSH, 1),
+            ("resnet50", "fp32", 25 * MIB, L.ALGO_AUTO, 2, {L.OPT_WIRE_BF16: 1}),     # N-3, vs O-8
+            ("toy", "fp32", 4096, L.ALGO_AUTO, 1, {L.OPT_WIRE_BF16: 1})]
     outs = _run(world, cfgs)
     for ci, cfg in enumerate(cfgs):
         model, dtype, cap, algo, iters = cfg[:5]
         ns = numels(model)
         algos = outs[0][ci][1]
         tol = any(x in ("nccl", "nvls") for x in algos)   # not rank-order sums: tolerance parity
+        wire = len(cfg) > 5 and cfg[5].get(L.OPT_WIRE_BF16)
         for it in range(iters):
             for p in range(len(ns)):
                 sums = [outs[r][ci][0][it][0][p] for r in range(world)]
@@ -122,7 +126,9 @@ def test_multigpu_parity(world):
                 idx = _sample_idx(p, ns[p])
                 got = outs[0][ci][0][it][1][p]
                 xs = [gen_values(15704, r, it, p, idx, "normal", dtype) for r in range(world)]
-                if tol:
+                if wire:
+                    assert np.array_equal(got, average_bf16_wire(xs)), (model, p)
+                elif tol:
                     ref, den = average_fp64(xs, dtype)
                     y = to_fp32(got, dtype).astype(np.float64)
                     r64 = to_fp32(ref, dtype).astype(np.float64)
