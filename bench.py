@@ -322,6 +322,8 @@ def run_ours(a):
         if kind == "p2p_fused" and world == 1:
             return 3 * (by["oneshot"] + by["twoshot"]), "hbm", "3 x bucket bytes (read g, write bucket, write g)"
         if kind == "pack":
+            if a.wire_bf16:
+                return 1.5 * by["ce"], "hbm", "fp32 read + bf16 write of every gradient (compressed wire)"
             return 2 * (by["nccl"] + small), "hbm", "2 x bytes packed (NCCL buckets; CE small gradients)"
         if kind == "unpack":
             return 2 * by["nccl"], "hbm", "2 x bucket bytes"
@@ -330,9 +332,13 @@ def run_ours(a):
                     + by["nvls"] * (1 + 1 / world), "nvlink",
                     "NVLink bytes per direction: one-shot (W-1)S, two-shot 2(W-1)/W S, NVLS (1+1/W)S")
         if kind == "ce_copy":
-            return ((by["ce"] + by["push"]) * (world - 1), "nvlink",
-                    "NVLink bytes per direction (W-1)S (copy engines / push kernel)")
+            wf = 0.5 if a.wire_bf16 else 1.0   # the compressed wire carries bf16
+            return ((by["ce"] * wf + by["push"]) * (world - 1), "nvlink",
+                    "NVLink bytes per direction (W-1)S_wire (copy engines / push kernel)")
         if kind == "ce_reduce":
+            if a.wire_bf16:
+                return (by["ce"] * (2 + (world - 1) / 2), "hbm",
+                        "own fp32 read + (W-1) bf16 slots + fp32 .grad write")
             return ((by["ce"] + by["push"]) * (world + 1), "hbm",
                     "(W+1) x bucket bytes (W operands read, .grad written)")
         return 2 * (world - 1) / world * by["nccl"], "nvlink", "ring 2(W-1)/W x bucket bytes"
@@ -523,15 +529,16 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
         torch.cuda.synchronize(dev)
         return s.elapsed_time(e)
 
-    def group(n: int) -> float:
-        """n-1 accumulating no_sync backward passes + 1 synced one: summed backward ms."""
+    def group(n: int, sync_last: bool = True) -> float:
+        """n-1 accumulating no_sync backward passes + 1 synced one (sync_last) or n
+        no_sync ones (the baseline with the same .grad accumulation): summed backward ms."""
         for p in ddp.params:
             p.grad = None
         tot = 0.0
         for k in range(n):
             loss = fwd(ddp)
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            if k < n - 1:
+            if k < n - 1 or not sync_last:
                 with ddp.no_sync():
                     s.record(stream)
                     loss.backward()
@@ -557,11 +564,15 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
             ddp.reducer.set_option(L.OPT_OVERLAP, 0)   # paper's non-overlapped baseline
             tn.append(one(True))
             ddp.reducer.set_option(L.OPT_OVERLAP, 1)
-    ns_res = {}
+    ns_res, ns_base = {}, {}
     for n in nosync_every:
         group(n)
-        gt = [group(n) for _ in range(max(2, iters // 2))]
-        ns_res[n] = statistics.median(gt)
+        group(n, False)
+        gt, gb = [], []
+        for _ in range(max(2, iters // 2)):
+            gt.append(group(n))
+            gb.append(group(n, False))
+        ns_res[n], ns_base[n] = statistics.median(gt), statistics.median(gb)
     # one profiled synced pass: Fig. 2(c)-style ready / start / end timeline of the comm launches
     ddp.reducer.set_option(L.OPT_PROFILE, 1)
     L.ddp_profile_timeline(ddp.reducer.ctx)
@@ -579,7 +590,7 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
                     if timeline_detail else None}
     ddp.reducer.check_errors()
     vals = [statistics.median(ts), statistics.median(tb), statistics.median(tn) if tn else 0.0]
-    vals += [ns_res[n] for n in nosync_every]
+    vals += [ns_res[n] for n in nosync_every] + [ns_base[n] for n in nosync_every]
     vt = torch.tensor(vals, dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vt, op=dist.ReduceOp.MAX)
@@ -594,9 +605,13 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
         res["t_bwd_plus_sync_no_overlap_ms"] = t_noov
         res["exposed_no_overlap_ms"] = t_noov - t_bwd
     if nosync_every:
+        k = len(nosync_every)
         res["nosync"] = {str(n): {"ms_per_iter": float(vt[3 + i]) / n,
-                                  "exposed_ms_per_iter": (float(vt[3 + i]) - n * t_bwd) / n}
+                                  "no_sync_baseline_ms_per_iter": float(vt[3 + k + i]) / n,
+                                  "exposed_ms_per_iter": (float(vt[3 + i]) - float(vt[3 + k + i])) / n}
                          for i, n in enumerate(nosync_every)}
+        res["nosync_doc"] = ("group of n backward passes with .grad accumulation: n-1 inside no_sync + 1 synced "
+                             "(ms_per_iter) vs all n inside no_sync (baseline); exposed = difference / n")
     ddp.close()
     return res
 

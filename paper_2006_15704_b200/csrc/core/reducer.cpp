@@ -88,7 +88,7 @@ struct ddp_ctx {
   // oneshot_max < 0: automatic (world 2: <= 1 MiB; world > 2: <= 512 KiB)
   int64_t overlap = 1, oneshot_max = -1, twoshot_max = INT64_MAX, comm_ctas = 64,
           dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 8, stage_bytes = 0,
-          find_unused = 0, multicast = 0, ce_streams = 4, nccl_comms = 1,
+          find_unused = 0, multicast = 0, ce_streams = 1, nccl_comms = 1,
           // CE: gradients of at least this many bytes travel straight from .grad (one
           // cudaMemcpyAsync per peer, a few us of host + copy-engine fixed cost each);
           // smaller ones are gathered into one region first (2x their bytes of HBM)
@@ -439,10 +439,14 @@ ddp_status_t launch_ce(ddp_ctx* c, int b) {
   // largest-first into the least loaded stream.
   const int K = push ? 0 : (int)c->ce_cp.size();
   if (!push) prof_begin(c, 4);
-  CUDA_TRY(c, cudaEventRecord(c->ce_go[b], c->comm));
+  if (K > 1) CUDA_TRY(c, cudaEventRecord(c->ce_go[b], c->comm));
   int64_t load[16] = {};
   bool used[16] = {};
   auto issue = [&](void* dst, const void* src, int64_t bytes) -> ddp_status_t {
+    if (K == 1) {  // one copy stream: the comm stream itself (no event hops)
+      CUDA_TRY(c, cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, c->comm));
+      return DDP_OK;
+    }
     int best = 0;
     for (int q = 1; q < K; ++q)
       if (load[q] < load[best]) best = q;
@@ -466,7 +470,7 @@ ddp_status_t launch_ce(ddp_ctx* c, int b) {
                                   (bk.ce_wire_numel - bk.ce_small0) * we))
         return st;
   }
-  for (int q = 0; q < K; ++q) {
+  for (int q = 0; q < K && K > 1; ++q) {
     if (!used[q]) continue;
     cudaEvent_t e = c->ce_cp_done[(size_t)b * K + q];
     CUDA_TRY(c, cudaEventRecord(e, c->ce_cp[q]));

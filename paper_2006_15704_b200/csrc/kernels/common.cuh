@@ -92,12 +92,12 @@ template <> struct Elem<__nv_bfloat16> {
 // EACH (with SCALE): every operand is scaled and rounded to T BEFORE the sum,
 //   y = RNE_T( sum_k RNE_T(src_k[i] * s) )        (oracle O-3b written out),
 // so raw gradients can be reduced with the 1/W of pack applied on the fly.
-template <typename T, int NS, int ND, bool SRC_NC, bool SCALE, bool EACH = false>
+template <typename T, int NS, int ND, bool SRC_NC, bool SCALE, bool EACH = false, int UF = 0>
 __device__ __forceinline__ void cta_xfer(T* const (&dst)[ND], const T* const (&src)[NS], int64_t n,
                                          float s) {
   using E = Elem<T>;
   constexpr int VE = E::VE;
-  constexpr int U = NS == 1 ? 8 : (NS >= 4 ? 1 : 4 / NS);
+  constexpr int U = UF ? UF : NS == 1 ? 8 : (NS >= 4 ? 1 : 4 / NS);
   const int tid = threadIdx.x, nt = blockDim.x;
   if (n <= 0) return;
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(dst[0]) & 15;

@@ -9,6 +9,8 @@
 // All buckets that become ready in the same call are one launch (their slots
 // concatenated into a virtual range split evenly over the CTAs), which removes
 // the per-bucket launch ramp of separate kernels.  HBM-bound.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace b200ddp {
@@ -23,7 +25,7 @@ struct GroupArgs {
   int32_t n;
 };
 
-template <typename T, int MAXS>
+template <typename T, int MAXS, int U>
 __global__ void __launch_bounds__(kThreads, 2)
     local_kernel(const __grid_constant__ GroupArgs<MAXS> ga, char* __restrict__ storage, int64_t chunk) {
   const int64_t total = ga.off[ga.n];
@@ -42,7 +44,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     T* g = static_cast<T*>(ga.grad[k]) + (x0 - s0);
     T* d[2] = {reinterpret_cast<T*>(storage + ga.dst[k]) + (x0 - s0), g};
     const T* sp[1] = {g};
-    cta_xfer<T, 1, 2, true, true>(d, sp, x1 - x0, 1.0f);
+    cta_xfer<T, 1, 2, true, true, false, U>(d, sp, x1 - x0, 1.0f);
   }
 }
 
@@ -63,7 +65,9 @@ cudaError_t run(const GroupView& gv, void* storage, int max_ctas, cudaStream_t s
   int64_t chunk = (total + ctas - 1) / ctas;
   chunk = (chunk + kAlignElems - 1) / kAlignElems * kAlignElems;
   ctas = (total + chunk - 1) / chunk;
-  local_kernel<T, MAXS><<<(int)ctas, kThreads, 0, st>>>(a, static_cast<char*>(storage), chunk);
+  static const int u = getenv("B200DDP_LOCAL_U") ? atoi(getenv("B200DDP_LOCAL_U")) : 8;  // experiment
+  if (u == 4) local_kernel<T, MAXS, 4><<<(int)ctas, kThreads, 0, st>>>(a, static_cast<char*>(storage), chunk);
+  else local_kernel<T, MAXS, 8><<<(int)ctas, kThreads, 0, st>>>(a, static_cast<char*>(storage), chunk);
   return cudaGetLastError();
 }
 
