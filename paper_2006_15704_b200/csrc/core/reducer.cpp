@@ -87,7 +87,9 @@ struct ddp_ctx {
   // options
   // oneshot_max < 0: automatic (world 2: <= 1 MiB; world > 2: <= 512 KiB)
   int64_t overlap = 1, oneshot_max = -1, twoshot_max = INT64_MAX, comm_ctas = 64,
-          dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO, pack_ctas = 148 * 8, stage_bytes = 0,
+          dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO,
+          pack_ctas = 148 * 32,  // many small CTAs balance best on HBM-bound copies (tools/local_probe.cu)
+          stage_bytes = 0,
           find_unused = 0, multicast = 0, ce_streams = 1, nccl_comms = 1,
           // CE: gradients of at least this many bytes travel straight from .grad (one
           // cudaMemcpyAsync per peer, a few us of host + copy-engine fixed cost each);

@@ -9,8 +9,6 @@
 // All buckets that become ready in the same call are one launch (their slots
 // concatenated into a virtual range split evenly over the CTAs), which removes
 // the per-bucket launch ramp of separate kernels.  HBM-bound.
-#include <cstdlib>
-
 #include "common.cuh"
 
 namespace b200ddp {
@@ -65,9 +63,7 @@ cudaError_t run(const GroupView& gv, void* storage, int max_ctas, cudaStream_t s
   int64_t chunk = (total + ctas - 1) / ctas;
   chunk = (chunk + kAlignElems - 1) / kAlignElems * kAlignElems;
   ctas = (total + chunk - 1) / chunk;
-  static const int u = getenv("B200DDP_LOCAL_U") ? atoi(getenv("B200DDP_LOCAL_U")) : 8;  // experiment
-  if (u == 4) local_kernel<T, MAXS, 4><<<(int)ctas, kThreads, 0, st>>>(a, static_cast<char*>(storage), chunk);
-  else local_kernel<T, MAXS, 8><<<(int)ctas, kThreads, 0, st>>>(a, static_cast<char*>(storage), chunk);
+  local_kernel<T, MAXS, 4><<<(int)ctas, kThreads, 0, st>>>(a, static_cast<char*>(storage), chunk);
   return cudaGetLastError();
 }
 
