@@ -94,10 +94,13 @@ enum {
   DDP_OPT_CE_DIRECT_BYTES = 14, /* CE algorithm: gradients >= this many bytes are copied straight
                                    from .grad (one copy per peer); smaller ones are gathered into
                                    one region first.  Default 16 MiB; layout key */
-  DDP_OPT_WIRE_BF16 = 15        /* compressed wire (§8(f) N-3): fp32 gradients travel
+  DDP_OPT_WIRE_BF16 = 15,       /* compressed wire (§8(f) N-3): fp32 gradients travel
                                    as bf16 through the CE exchange (every bucket uses DDP_ALGO_CE at
                                    world > 1): s_q = RNE_bf16(g_q * fl(1/W)), fp32 rank-order sum,
                                    fp32 result (oracle O-8).  fp32 contexts only; layout key */
+  DDP_OPT_LANES = 16            /* P2P / NVLS kernels of bucket b run on stream (lane) b mod LANES,
+                                   each lane with its own barrier flags, sequence and staging, so
+                                   consecutive buckets' kernels overlap.  1..4, default 2; layout key */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.

@@ -45,6 +45,7 @@ constexpr int64_t kMinChunkElems = 4096;   // smallest per-CTA chunk worth a CTA
 // stage per chunk (one sync for one-shot, two for two-shot); DDP_OPT_P2P_STAGE_BYTES
 // splits chunks for experiments.
 constexpr int64_t kBarrierScratch = 32 * 1024;  // scratch int inside the flags region
+constexpr int kMaxLanes = 4;
 constexpr int64_t kCeWireAlign = 64;  // elements: wire offsets keep 16-B (and 256-B) alignment
 
 struct Bucket {
@@ -95,7 +96,11 @@ struct ddp_ctx {
           // cudaMemcpyAsync per peer, a few us of host + copy-engine fixed cost each);
           // smaller ones are gathered into one region first (2x their bytes of HBM)
           ce_direct = 16 << 20,
-          wire_bf16 = 0;  // N-3: fp32 gradients travel as bf16 (CE exchange)
+          wire_bf16 = 0,  // N-3: fp32 gradients travel as bf16 (CE exchange)
+          // P2P / NVLS kernels of consecutive buckets run on `lanes` streams (bucket b on
+          // lane b mod lanes), each with its own barrier flags, sequence and staging, so
+          // bucket b+1's local phases overlap bucket b's NVLink phase
+          lanes = 2;
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
           stage1_stride = 0, ce_flags_off = 0, bitmap_off = 0, scratch_off = 0, storage_bytes = 0;
@@ -148,8 +153,11 @@ struct ddp_ctx {
   std::vector<cudaStream_t> unwaited;  // producer streams since the last event wait
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> stream_events;
   cudaEvent_t comm_done = nullptr;
-  uint32_t p2p_seq = 1;
-  uint64_t p2p_launches = 0;
+  uint32_t p2p_seq[kMaxLanes] = {1, 1, 1, 1};
+  uint64_t p2p_launches[kMaxLanes] = {};
+  cudaStream_t lane_stream[kMaxLanes] = {};  // [0] = comm
+  cudaEvent_t lane_done[kMaxLanes] = {};
+  bool lane_used[kMaxLanes] = {};
   uint32_t* err_host = nullptr;
   uint32_t* err_dev = nullptr;
   std::vector<ProfRec> prof;
@@ -273,7 +281,7 @@ int max_ctas_for(const ddp_ctx* c, const Bucket& bk) {
 }
 
 void plan(ddp_ctx* c) {
-  int64_t pos = kFlagsBytes;
+  int64_t pos = c->lanes * kFlagsBytes;  // one flag table per lane
   c->flags_off = 0;
   c->buckets_off = pos;
   int64_t l2max = 0, n1max = 0;
@@ -286,10 +294,10 @@ void plan(ddp_ctx* c) {
   }
   c->stage2_stride = align_up(l2max * c->esize, 256);
   c->stage2_off = pos;
-  pos += c->world * c->stage2_stride;
+  pos += c->lanes * c->world * c->stage2_stride;  // per lane
   c->stage1_stride = align_up(n1max * c->esize, 256);
   c->stage1_off = pos;
-  pos += 2 * c->world * c->stage1_stride;  // double-buffered by launch parity
+  pos += c->lanes * 2 * c->world * c->stage1_stride;  // per lane, double-buffered by the lane's launch parity
   // copy-engine buckets: W slots each (dedicated per bucket) + ready/consumed flags
   c->ce_flags_off = pos;
   pos += align_up((int64_t)c->buckets.size() * kMaxWorld * 2 * 4, 256);
@@ -325,7 +333,7 @@ void plan(ddp_ctx* c) {
     c->bitmap_off = pos;
     pos += align_up((int64_t)c->numel.size() * 4, 256);
     c->scratch_off = pos;
-    pos += c->stage2_off - c->buckets_off;
+    pos += c->stage2_off - c->buckets_off;  // = the bucket region
   }
   c->storage_bytes = pos;
   for (Bucket& bk : c->buckets) grid_for(c, bk, max_ctas_for(c, bk));
@@ -533,18 +541,26 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
     prof_end(c, s);
     return DDP_OK;
   }
+  // lane: its stream, flag table, sequence and staging (identical choice on every rank)
+  // Lanes run spinning kernels side by side: all of them must fit on the SMs at
+  // once (one CTA per SM guaranteed), else a lane could wait for a peer lane that
+  // cannot be scheduled.  Same options on every rank -> same choice everywhere.
+  const int nl = c->lanes * std::min<int64_t>(c->comm_ctas, kMaxCtas) <= 148 ? (int)c->lanes : 1;
+  const int ln = (c->emulated || c->world == 1) ? 0 : b % nl;
+  cudaStream_t ls = ln == 0 ? c->comm : c->lane_stream[ln];
+  if (ln) c->lane_used[ln] = true;
   P2PLaunch a{};
   for (int r = 0; r < c->world; ++r) a.storage[r] = c->storage[r];
-  a.flags_byte_off = c->flags_off;
+  a.flags_byte_off = c->flags_off + ln * kFlagsBytes;
   a.bucket_byte_off = bk.byte_off;
   if (bk.algo == DDP_ALGO_TWOSHOT) {
-    a.stage_byte_off = c->stage2_off;
+    a.stage_byte_off = c->stage2_off + ln * c->world * c->stage2_stride;
     a.stage_stride = c->stage2_stride;
   } else if (c->world == 1) {
     a.stage_byte_off = bk.byte_off;  // world 1 packs straight into the bucket
     a.stage_stride = 0;
   } else {
-    a.stage_byte_off = c->stage1_off + (int64_t)(c->p2p_launches & 1) * c->world * c->stage1_stride;
+    a.stage_byte_off = c->stage1_off + (int64_t)(2 * ln + (c->p2p_launches[ln] & 1)) * c->world * c->stage1_stride;
     a.stage_stride = c->stage1_stride;
   }
   a.numel = bk.numel;
@@ -556,17 +572,17 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   a.emulated = c->emulated ? 1 : 0;
   a.sub = bk.sub;
   a.stages = bk.stages;
-  a.seq = c->p2p_seq;
+  a.seq = c->p2p_seq[ln];
   a.scale = scale;
   a.grad_rank_stride = c->grad_rank_stride;
   a.err = c->err_dev;
   a.mc = c->mc;
-  c->p2p_seq += (uint32_t)bk.stages + 2;  // flag values used: seq .. seq + stages + 1
-  c->p2p_launches += 1;
-  prof_begin(c, 3);
-  if (bk.algo == DDP_ALGO_NVLS) CUDA_TRY(c, launch_nvls(c->dtype, sv, a, c->comm));
-  else CUDA_TRY(c, launch_p2p(bk.algo, c->dtype, sv, a, c->comm));
-  prof_end(c);
+  c->p2p_seq[ln] += (uint32_t)bk.stages + 2;  // flag values used: seq .. seq + stages + 1
+  c->p2p_launches[ln] += 1;
+  prof_begin(c, 3, ls);
+  if (bk.algo == DDP_ALGO_NVLS) CUDA_TRY(c, launch_nvls(c->dtype, sv, a, ls));
+  else CUDA_TRY(c, launch_p2p(bk.algo, c->dtype, sv, a, ls));
+  prof_end(c, ls);
   return DDP_OK;
 }
 
@@ -632,6 +648,8 @@ ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
     CUDA_TRY(c, cudaStreamWaitEvent(c->comm, ev, 0));
     if (c->ce_pack) CUDA_TRY(c, cudaStreamWaitEvent(c->ce_pack, ev, 0));
     for (size_t k = 1; k < c->rr_stream.size(); ++k) CUDA_TRY(c, cudaStreamWaitEvent(c->rr_stream[k], ev, 0));
+    for (int k = 1; k < kMaxLanes; ++k)
+      if (c->lane_stream[k]) CUDA_TRY(c, cudaStreamWaitEvent(c->lane_stream[k], ev, 0));
     for (cudaStream_t q : c->ce_cp) CUDA_TRY(c, cudaStreamWaitEvent(q, ev, 0));
   }
   c->unwaited.clear();
@@ -756,7 +774,7 @@ ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s, b
 bool is_layout_key(int32_t k) {
   return k == DDP_OPT_P2P_ONESHOT_MAX || k == DDP_OPT_P2P_TWOSHOT_MAX || k == DDP_OPT_ALGO ||
          k == DDP_OPT_FIND_UNUSED || k == DDP_OPT_MULTICAST || k == DDP_OPT_CE_DIRECT_BYTES ||
-         k == DDP_OPT_WIRE_BF16;
+         k == DDP_OPT_WIRE_BF16 || k == DDP_OPT_LANES;
 }
 
 }  // namespace
@@ -851,6 +869,13 @@ void ddp_destroy(ddp_ctx_t* c) {
     cudaStreamDestroy(s);
   }
   for (cudaEvent_t e : c->ce_go) cudaEventDestroy(e);
+  for (int k = 1; k < kMaxLanes; ++k) {
+    if (c->lane_stream[k]) {
+      if (!c->poisoned) cudaStreamSynchronize(c->lane_stream[k]);
+      cudaStreamDestroy(c->lane_stream[k]);
+    }
+    if (c->lane_done[k]) cudaEventDestroy(c->lane_done[k]);
+  }
   for (cudaEvent_t e : c->ce_cp_done) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ce_packed) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ce_copied) cudaEventDestroy(e);
@@ -960,7 +985,15 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
     }
   }
   char* mine = static_cast<char*>(c->storage[c->rank]);
-  CUDA_TRY(c, cudaMemsetAsync(mine + c->flags_off, 0, kFlagsBytes, c->comm));
+  CUDA_TRY(c, cudaMemsetAsync(mine + c->flags_off, 0, c->lanes * kFlagsBytes, c->comm));
+  if (c->world > 1 && c->lanes > 1) {
+    int lo = 0, hi = 0;
+    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (int k = 1; k < c->lanes; ++k) {
+      CUDA_TRY(c, cudaStreamCreateWithPriority(&c->lane_stream[k], cudaStreamNonBlocking, hi));
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->lane_done[k], cudaEventDisableTiming));
+    }
+  }
   CUDA_TRY(c, cudaMemsetAsync(mine + c->ce_flags_off, 0, (size_t)c->buckets.size() * kMaxWorld * 2 * 4, c->comm));
   bool any_ce = false;
   for (const Bucket& bk : c->buckets) any_ce |= bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH;
@@ -1016,7 +1049,7 @@ ddp_status_t ddp_bind_emulated(ddp_ctx_t* c, int32_t device, void* comm_stream, 
   c->emulated = true;
   regrid(c);
   for (int r = 0; r < c->world; ++r)
-    CUDA_TRY(c, cudaMemsetAsync(static_cast<char*>(c->storage[r]) + c->flags_off, 0, kFlagsBytes, c->comm));
+    CUDA_TRY(c, cudaMemsetAsync(static_cast<char*>(c->storage[r]) + c->flags_off, 0, c->lanes * kFlagsBytes, c->comm));
   CUDA_TRY(c, cudaStreamSynchronize(c->comm));
   c->bound = true;
   c->state = State::IDLE;
@@ -1095,6 +1128,12 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
         CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->rr_done[k], 0));
         c->rr_used[k] = 0;
       }
+      for (int k = 1; k < kMaxLanes; ++k) {
+        if (!c->lane_used[k]) continue;
+        CUDA_TRY(c, cudaEventRecord(c->lane_done[k], c->lane_stream[k]));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->lane_done[k], 0));
+        c->lane_used[k] = false;
+      }
     }
     if (c->find_unused) {
       if (!c->dry_run) {
@@ -1165,6 +1204,10 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       if (v < 0) return fail(DDP_ERR_INVALID_ARG, "negative CE_DIRECT_BYTES");
       c->ce_direct = v;
       break;
+    case DDP_OPT_LANES:
+      if (v < 1 || v > kMaxLanes) return fail(DDP_ERR_INVALID_ARG, "LANES must be in [1, 4]");
+      c->lanes = v;
+      break;
     case DDP_OPT_WIRE_BF16:
       if (v && c->dtype != DDP_FP32) return fail(DDP_ERR_INVALID_ARG, "WIRE_BF16 compresses fp32 gradients only");
       c->wire_bf16 = v ? 1 : 0;
@@ -1219,6 +1262,7 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_NCCL_COMMS: *v = c->nccl_comms; break;
     case DDP_OPT_CE_DIRECT_BYTES: *v = c->ce_direct; break;
     case DDP_OPT_WIRE_BF16: *v = c->wire_bf16; break;
+    case DDP_OPT_LANES: *v = c->lanes; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;

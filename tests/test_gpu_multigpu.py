@@ -111,7 +111,10 @@ def test_multigpu_parity(world):
             ("toy", "fp32", 4096, L.ALGO_PUSH, 3), ("resnet50", "bf16", 25 * MIB, L.ALGO_PUSH, 2),
             ("bert_large", "fp32", 25 * MIB, L.ALGO_PUSH, 1),
             ("resnet50", "fp32", 25 * MIB, L.ALGO_AUTO, 2, {L.OPT_WIRE_BF16: 1}),     # N-3, vs O-8
-            ("toy", "fp32", 4096, L.ALGO_AUTO, 1, {L.OPT_WIRE_BF16: 1})]
+            ("toy", "fp32", 4096, L.ALGO_AUTO, 1, {L.OPT_WIRE_BF16: 1}),
+            ("resnet50", "fp32", 1 * MIB, L.ALGO_TWOSHOT, 2, {L.OPT_LANES: 4, L.OPT_COMM_CTAS: 32}),
+            ("resnet50", "bf16", 1 * MIB, L.ALGO_ONESHOT, 3, {L.OPT_LANES: 3, L.OPT_COMM_CTAS: 16}),
+            ("resnet50", "fp32", 5 * MIB, L.ALGO_ONESHOT, 2, {L.OPT_LANES: 1})]
     outs = _run(world, cfgs)
     for ci, cfg in enumerate(cfgs):
         model, dtype, cap, algo, iters = cfg[:5]
