@@ -235,14 +235,15 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
     a = DDP_ALGO_ONESHOT;
   } else if (c->wire_bf16) {
     a = DDP_ALGO_CE;
-  } else if (bytes <= (c->oneshot_max >= 0 ? c->oneshot_max : c->world == 2 ? (1 << 20) : 512 * 1024)) {
+  } else if (bytes <= (c->oneshot_max >= 0 ? c->oneshot_max : (1 << 20))) {
     a = DDP_ALGO_ONESHOT;  // latency-bound: one fused kernel, one barrier
   } else if (bytes <= c->twoshot_max) {
     // world 2: the copy-engine exchange moves the same (W-1) S = S bytes as any
     // algorithm, keeps the SMs free for backward and pipelines buckets
-    // (profiles/r01_n2.md); wider: fewer NVLink bytes win — NVLS (1+1/W) S, else
-    // two-shot 2(W-1)/W S
-    a = c->world == 2 ? DDP_ALGO_CE : c->multicast ? DDP_ALGO_NVLS : DDP_ALGO_TWOSHOT;
+    // (profiles/r01_n2.md).  Wider: two-shot, 2(W-1)/W S per direction (best
+    // measured at W=4, profiles/r01_n4.md); from W=6 NVLS's (1+1/W) S is >= 1.5x
+    // fewer NVLink bytes, which outweighs its lower per-byte rate seen at W=4
+    a = c->world == 2 ? DDP_ALGO_CE : (c->multicast && c->world >= 6) ? DDP_ALGO_NVLS : DDP_ALGO_TWOSHOT;
   } else {
     a = DDP_ALGO_NCCL;
   }
