@@ -318,7 +318,7 @@ def run_ours(a):
             for s_ in range(L.ddp_bucket_info(red.ctx, b)[1]):
                 p, _ = L.ddp_bucket_slot(red.ctx, b, s_)
                 small += ns[p] * esize if ns[p] * esize < L.ddp_get_option(red.ctx, L.OPT_CE_DIRECT_BYTES) else 0
-    by = {x: sum(n * esize for n, y in zip(bnumel, algos) if y == x) for x in ("nccl", "oneshot", "twoshot", "ce", "nvls", "push")}
+    by = {x: sum(n * esize for n, y in zip(bnumel, algos) if y == x) for x in ("nccl", "oneshot", "twoshot", "ce", "nvls", "push", "ce2")}
 
     def kind_bytes(kind):
         """(algorithmic bytes per step, bound, rule) of one profile kind."""
@@ -327,23 +327,24 @@ def run_ours(a):
         if kind == "pack":
             if a.wire_bf16:
                 return 1.5 * by["ce"], "hbm", "fp32 read + bf16 write of every gradient (compressed wire)"
-            return 2 * (by["nccl"] + small), "hbm", "2 x bytes packed (NCCL buckets; CE small gradients)"
+            return (2 * (by["nccl"] + small + by["ce2"]), "hbm",
+                    "2 x bytes packed (NCCL and CE2 buckets; CE small gradients)")
         if kind == "unpack":
-            return 2 * by["nccl"], "hbm", "2 x bucket bytes"
+            return 2 * (by["nccl"] + by["ce2"]), "hbm", "2 x bucket bytes"
         if kind == "p2p_fused":
             return (by["oneshot"] * (world - 1) + by["twoshot"] * 2 * (world - 1) / world
                     + by["nvls"] * (1 + 1 / world), "nvlink",
                     "NVLink bytes per direction: one-shot (W-1)S, two-shot 2(W-1)/W S, NVLS (1+1/W)S")
         if kind == "ce_copy":
             wf = 0.5 if a.wire_bf16 else 1.0   # the compressed wire carries bf16
-            return ((by["ce"] * wf + by["push"]) * (world - 1), "nvlink",
-                    "NVLink bytes per direction (W-1)S_wire (copy engines / push kernel)")
+            return ((by["ce"] * wf + by["push"]) * (world - 1) + by["ce2"] * 2 * (world - 1) / world, "nvlink",
+                    "NVLink bytes per direction: CE/PUSH (W-1)S_wire, CE2 2(W-1)/W S (copy engines / push kernel)")
         if kind == "ce_reduce":
             if a.wire_bf16:
                 return (by["ce"] * (2 + (world - 1) / 2), "hbm",
                         "own fp32 read + (W-1) bf16 slots + fp32 .grad write")
-            return ((by["ce"] + by["push"]) * (world + 1), "hbm",
-                    "(W+1) x bucket bytes (W operands read, .grad written)")
+            return ((by["ce"] + by["push"]) * (world + 1) + by["ce2"] * (world + 1) / world, "hbm",
+                    "(W+1) x bucket bytes (W operands read, .grad written); CE2 (W+1)/W S (one shard)")
         return 2 * (world - 1) / world * by["nccl"], "nvlink", "ring 2(W-1)/W x bucket bytes"
 
     def roof_of(kind):

@@ -117,6 +117,9 @@ struct ddp_ctx {
   bool bitmap_valid = false;
   // copy-engine path: reduce stream, events, driver stream-memory-op entry points
   cudaStream_t ce_red = nullptr, ce_pack = nullptr;
+  cudaStream_t ce_ag = nullptr, ce_up = nullptr;  // CE2: all-gather copies, unpack
+  std::vector<cudaEvent_t> ce_reduced;             // CE2, per bucket: own shard reduced
+  bool ce2_used = false;
   std::vector<cudaStream_t> ce_cp;          // copy streams: copies of one bucket spread over them
   std::vector<cudaEvent_t> ce_go;           // per bucket: copies may start (comm -> copy streams)
   std::vector<cudaEvent_t> ce_cp_done;      // per bucket x copy stream: its copies issued
@@ -228,7 +231,8 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   int a;
   if (c->algo != DDP_ALGO_AUTO) {
     a = (int)c->algo;
-    if (c->world == 1 && (a == DDP_ALGO_CE || a == DDP_ALGO_NVLS || a == DDP_ALGO_PUSH)) a = DDP_ALGO_ONESHOT;
+    if (c->world == 1 && (a == DDP_ALGO_CE || a == DDP_ALGO_NVLS || a == DDP_ALGO_PUSH || a == DDP_ALGO_CE2))
+      a = DDP_ALGO_ONESHOT;
     if (c->world > 1 && c->wire_bf16) a = DDP_ALGO_CE;  // the compressed wire is a CE feature
     if (a == DDP_ALGO_NVLS && !c->multicast) a = DDP_ALGO_TWOSHOT;
   } else if (c->world == 1) {
@@ -255,9 +259,10 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
 
 // Grid of a P2P launch: per-CTA chunks of >= kMinChunkElems, 256-element aligned.
 void grid_for(const ddp_ctx* c, Bucket& bk, int max_ctas) {
-  if (bk.algo == DDP_ALGO_NCCL) {
+  if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE2) {
     bk.ctas = 0;
-    bk.shard = bk.chunk = 0;
+    bk.chunk = 0;
+    if (bk.algo == DDP_ALGO_NCCL) bk.shard = 0;
     return;
   }
   const bool sharded = bk.algo == DDP_ALGO_TWOSHOT || bk.algo == DDP_ALGO_NVLS;
@@ -301,11 +306,19 @@ void plan(ddp_ctx* c) {
   pos += c->lanes * 2 * c->world * c->stage1_stride;  // per lane, double-buffered by the lane's launch parity
   // copy-engine buckets: W slots each (dedicated per bucket) + ready/consumed flags
   c->ce_flags_off = pos;
-  pos += align_up((int64_t)c->buckets.size() * kMaxWorld * 2 * 4, 256);
+  pos += align_up((int64_t)c->buckets.size() * kMaxWorld * 3 * 4, 256);  // kinds: ready, consumed, gathered
   for (Bucket& bk : c->buckets) {
     bk.ce_stride = 0;
     bk.ce_wire.clear();
     bk.ce_direct.clear();
+    if (bk.algo == DDP_ALGO_CE2) {  // double-buffered reduce-scatter staging: [2][W] shard slots
+      const int64_t L = align_up(cdiv(bk.numel, c->world), kAlignElems);
+      bk.shard = L;
+      bk.ce_stride = align_up(L * c->esize, 256);
+      bk.ce_off = pos;
+      pos += 2 * c->world * bk.ce_stride;
+      continue;
+    }
     if (bk.algo != DDP_ALGO_CE && bk.algo != DDP_ALGO_PUSH) continue;
     const size_t ns = bk.params.size();
     bk.ce_wire.assign(ns, 0);
@@ -517,6 +530,79 @@ ddp_status_t launch_ce(ddp_ctx* c, int b) {
   return DDP_OK;
 }
 
+// Copy-engine two-shot (CE2): the reduce-scatter and all-gather of a ring /
+// two-shot, 2 (W-1)/W S NVLink bytes per direction, moved by copy engines and
+// ordered by stream memory operations (no SM waits):
+//   pack stream:    pack x 1/W into the own bucket
+//   comm stream:    shard j of the own bucket -> peer j's staging slot r (half v%2);
+//                   ready flags
+//   reduce stream:  [wait all ready] own shard = rank-order sum of the W values
+//                   (slot q, own bucket for q = r), in place in the own bucket
+//   all-gather:     [after the reduce] own shard -> shard r of every peer's bucket;
+//                   gathered flags
+//   unpack stream:  [wait all gathered] own bucket -> .grad
+// Staging is double-buffered by pass parity, so no "consumed" flags are needed:
+// writing half v%2 again (pass v+2) follows, through this rank's own finalize,
+// every peer's all-gather of pass v+1, which follows its reduce of pass v.
+ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
+  Bucket& bk = c->buckets[b];
+  const int W = c->world, r = c->rank;
+  const uint32_t v = ++bk.ce_count;
+  char* mine = static_cast<char*>(c->storage[r]);
+  char* own = mine + bk.byte_off;
+  const int64_t L = bk.shard, e = c->esize;
+  const int64_t half = (int64_t)(v & 1) * W * bk.ce_stride;
+  auto shard_len = [&](int j) { return std::max<int64_t>(0, std::min<int64_t>(L, bk.numel - j * L)); };
+  prof_begin(c, 0, c->ce_pack);
+  CUDA_TRY(c, launch_pack(c->dtype, sv, own, scale, (int)c->pack_ctas, c->ce_pack));
+  prof_end(c, c->ce_pack);
+  CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_packed[b], 0));
+  prof_begin(c, 4);
+  for (int i = 1; i < W; ++i) {
+    const int j = (r + i) % W;
+    if (shard_len(j) > 0)
+      CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->storage[j]) + bk.ce_off + half + r * bk.ce_stride,
+                                  own + j * L * e, (size_t)(shard_len(j) * e), cudaMemcpyDeviceToDevice, c->comm));
+  }
+  prof_end(c);
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_write(c, c->comm, ce_flag(c, (r + i) % W, 0, b, r), v)) return st;
+  // reduce own shard r in rank order
+  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_red, c->ce_packed[b], 0));
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_wait(c, c->ce_red, ce_flag(c, r, 0, b, (r + i) % W), v)) return st;
+  const void* src[kMaxWorld];
+  for (int q = 0; q < W; ++q)
+    src[q] = q == r ? static_cast<const void*>(own + r * L * e)
+                    : static_cast<const void*>(mine + bk.ce_off + half + q * bk.ce_stride);
+  prof_begin(c, 5, c->ce_red);
+  CUDA_TRY(c, launch_shard_reduce(c->dtype, W, src, own + r * L * e, shard_len(r), (int)c->pack_ctas, c->ce_red));
+  prof_end(c, c->ce_red);
+  CUDA_TRY(c, cudaEventRecord(c->ce_reduced[b], c->ce_red));
+  // all-gather the reduced own shard into every peer's bucket
+  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_ag, c->ce_reduced[b], 0));
+  prof_begin(c, 4, c->ce_ag);
+  for (int i = 1; i < W; ++i) {
+    const int j = (r + i) % W;
+    if (shard_len(r) > 0)
+      CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->storage[j]) + bk.byte_off + r * L * e, own + r * L * e,
+                                  (size_t)(shard_len(r) * e), cudaMemcpyDeviceToDevice, c->ce_ag));
+  }
+  prof_end(c, c->ce_ag);
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_write(c, c->ce_ag, ce_flag(c, (r + i) % W, 2, b, r), v)) return st;
+  // unpack once every shard has arrived
+  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_up, c->ce_reduced[b], 0));
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_wait(c, c->ce_up, ce_flag(c, r, 2, b, (r + i) % W), v)) return st;
+  prof_begin(c, 2, c->ce_up);
+  CUDA_TRY(c, launch_unpack(c->dtype, sv, own, (int)c->pack_ctas, c->ce_up));
+  prof_end(c, c->ce_up);
+  c->ce2_used = true;
+  return DDP_OK;
+}
+
 // ---- a3/a4/a6 device work for one bucket -------------------------------------
 ddp_status_t launch_device(ddp_ctx* c, int b) {
   Bucket& bk = c->buckets[b];
@@ -524,6 +610,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   const float scale = 1.0f / (float)c->world;  // fl(1/W), reading C-2
   char* mine = static_cast<char*>(c->storage[c->rank]);
   if (bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH) return launch_ce(c, b);
+  if (bk.algo == DDP_ALGO_CE2) return launch_ce2(c, b, sv, scale);
   if (bk.algo == DDP_ALGO_NCCL) {
     void* buf = mine + bk.byte_off;
     const size_t k = c->rr_comm.empty() ? 0 : (size_t)b % c->rr_comm.size();
@@ -648,6 +735,7 @@ ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
     CUDA_TRY(c, cudaEventRecord(ev, s));
     CUDA_TRY(c, cudaStreamWaitEvent(c->comm, ev, 0));
     if (c->ce_pack) CUDA_TRY(c, cudaStreamWaitEvent(c->ce_pack, ev, 0));
+    if (c->ce_up) CUDA_TRY(c, cudaStreamWaitEvent(c->ce_up, ev, 0));  // unpack writes .grad
     for (size_t k = 1; k < c->rr_stream.size(); ++k) CUDA_TRY(c, cudaStreamWaitEvent(c->rr_stream[k], ev, 0));
     for (int k = 1; k < kMaxLanes; ++k)
       if (c->lane_stream[k]) CUDA_TRY(c, cudaStreamWaitEvent(c->lane_stream[k], ev, 0));
@@ -862,6 +950,8 @@ void ddp_destroy(ddp_ctx_t* c) {
   for (cudaEvent_t e : c->prof_ready) cudaEventDestroy(e);
   if (c->comm_done) cudaEventDestroy(c->comm_done);
   std::vector<cudaStream_t> own = c->ce_cp;
+  own.push_back(c->ce_ag);
+  own.push_back(c->ce_up);
   own.push_back(c->ce_red);
   own.push_back(c->ce_pack);
   for (cudaStream_t s : own) {
@@ -870,6 +960,7 @@ void ddp_destroy(ddp_ctx_t* c) {
     cudaStreamDestroy(s);
   }
   for (cudaEvent_t e : c->ce_go) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ce_reduced) cudaEventDestroy(e);
   for (int k = 1; k < kMaxLanes; ++k) {
     if (c->lane_stream[k]) {
       if (!c->poisoned) cudaStreamSynchronize(c->lane_stream[k]);
@@ -995,9 +1086,10 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
       CUDA_TRY(c, cudaEventCreateWithFlags(&c->lane_done[k], cudaEventDisableTiming));
     }
   }
-  CUDA_TRY(c, cudaMemsetAsync(mine + c->ce_flags_off, 0, (size_t)c->buckets.size() * kMaxWorld * 2 * 4, c->comm));
+  CUDA_TRY(c, cudaMemsetAsync(mine + c->ce_flags_off, 0, (size_t)c->buckets.size() * kMaxWorld * 3 * 4, c->comm));
   bool any_ce = false;
-  for (const Bucket& bk : c->buckets) any_ce |= bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH;
+  for (const Bucket& bk : c->buckets)
+    any_ce |= bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH || bk.algo == DDP_ALGO_CE2;
   if (any_ce) {
     int lo = 0, hi = 0;
     CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -1007,6 +1099,10 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
     for (auto& e : c->ce_packed) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->ce_copied.assign(c->buckets.size(), nullptr);
     for (auto& e : c->ce_copied) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_ag, cudaStreamNonBlocking, hi));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_up, cudaStreamNonBlocking, hi));
+    c->ce_reduced.assign(c->buckets.size(), nullptr);
+    for (auto& e : c->ce_reduced) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->ce_cp.assign((size_t)c->ce_streams, nullptr);
     for (auto& q : c->ce_cp) CUDA_TRY(c, cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
     c->ce_go.assign(c->buckets.size(), nullptr);
@@ -1040,7 +1136,7 @@ ddp_status_t ddp_bind_emulated(ddp_ctx_t* c, int32_t device, void* comm_stream, 
       return fail(DDP_ERR_INVALID_ARG, "storages must be non-null and 256-B aligned");
   }
   for (const Bucket& bk : c->buckets)
-    if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH)
+    if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH || bk.algo == DDP_ALGO_CE2)
       return fail(DDP_ERR_UNSUPPORTED, "emulation runs the one-shot / two-shot kernels only (set DDP_OPT_ALGO)");
   if (c->find_unused) return fail(DDP_ERR_UNSUPPORTED, "find_unused needs a real communicator (no emulation)");
   if (c->multicast) return fail(DDP_ERR_UNSUPPORTED, "NVLS needs real multicast memory (no emulation)");
@@ -1123,6 +1219,11 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
         CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_red_done, 0));
         c->ce_used = false;
       }
+      if (c->ce2_used) {  // CE2 writes .grad on the unpack stream
+        CUDA_TRY(c, cudaEventRecord(c->ce_red_done, c->ce_up));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_red_done, 0));
+        c->ce2_used = false;
+      }
       for (size_t k = 1; k < c->rr_stream.size(); ++k) {
         if (!c->rr_used[k]) continue;
         CUDA_TRY(c, cudaEventRecord(c->rr_done[k], c->rr_stream[k]));
@@ -1192,7 +1293,7 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       c->twoshot_max = v;
       break;
     case DDP_OPT_ALGO:
-      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_PUSH) return fail(DDP_ERR_INVALID_ARG, "bad algo");
+      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_CE2) return fail(DDP_ERR_INVALID_ARG, "bad algo");
       c->algo = v;
       break;
     case DDP_OPT_FIND_UNUSED:

@@ -152,7 +152,7 @@ def _worker(rank, world, init_file, algo, q):
 
 @pytest.mark.multigpu
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("algo", [2, 3, 4, 6, 1])   # one-shot, two-shot, CE, push, NCCL
+@pytest.mark.parametrize("algo", [2, 3, 4, 6, 7, 1])   # one-shot, two-shot, CE, push, CE2, NCCL
 def test_world2_unused_vs_oracle(algo):
     world = 2
     ctx = mp.get_context("spawn")
