@@ -70,7 +70,7 @@ enum {
   DDP_OPT_P2P_ONESHOT_MAX = 2,  /* buckets <= this many bytes use the one-shot P2P kernel */
   DDP_OPT_P2P_TWOSHOT_MAX = 3,  /* buckets <= this many bytes use the two-shot P2P kernel; larger
                                    buckets use NCCL */
-  DDP_OPT_COMM_CTAS = 4,        /* max CTAs of a P2P kernel when world > 1 (1..148) */
+  DDP_OPT_COMM_CTAS = 4,        /* max CTAs of a P2P kernel when world > 1 (1..148, default 32) */
   DDP_OPT_DRY_RUN = 5,          /* 1: protocol only, no device work (host tests; CREATED only) */
   DDP_OPT_PROFILE = 6,          /* 1: time every device launch with CUDA events */
   DDP_OPT_ALGO = 7,             /* force the bucket allreduce: 0 auto, 1 NCCL, 2 one-shot, 3 two-shot,
@@ -100,7 +100,9 @@ enum {
                                    fp32 result (oracle O-8).  fp32 contexts only; layout key */
   DDP_OPT_LANES = 16            /* P2P / NVLS kernels of bucket b run on stream (lane) b mod LANES,
                                    each lane with its own barrier flags, sequence and staging, so
-                                   consecutive buckets' kernels overlap.  1..4, default 2; layout key */
+                                   consecutive buckets' kernels overlap.  1..4, default 4; layout key.
+                                   Lanes are used only while LANES x COMM_CTAS <= 148 (all lanes'
+                                   spinning kernels must fit on the SMs at once) */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.

@@ -87,7 +87,8 @@ struct ddp_ctx {
   std::vector<int64_t> p_off;
   // options
   // oneshot_max < 0: automatic (world 2: <= 1 MiB; world > 2: <= 512 KiB)
-  int64_t overlap = 1, oneshot_max = -1, twoshot_max = INT64_MAX, comm_ctas = 64,
+  int64_t overlap = 1, oneshot_max = -1, twoshot_max = INT64_MAX,
+          comm_ctas = 32,  // x 4 lanes: measured best exposed time at W=4 (profiles/r01_n4.md)
           dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO,
           pack_ctas = 148 * 32,  // many small CTAs balance best on HBM-bound copies (tools/local_probe.cu)
           stage_bytes = 0,
@@ -100,7 +101,7 @@ struct ddp_ctx {
           // P2P / NVLS kernels of consecutive buckets run on `lanes` streams (bucket b on
           // lane b mod lanes), each with its own barrier flags, sequence and staging, so
           // bucket b+1's local phases overlap bucket b's NVLink phase
-          lanes = 2;
+          lanes = 4;
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
           stage1_stride = 0, ce_flags_off = 0, bitmap_off = 0, scratch_off = 0, storage_bytes = 0;
