@@ -328,7 +328,11 @@ def run_ours(a):
     # dominant kernel roofline: algorithmic bytes per launch / measured launch time
     peak_hbm, peak_src = measured_peaks()
     kinds = {k: v for k, v in prof.items() if v[1] > 0}
-    dom = max(kinds, key=lambda k: kinds[k][2]) if kinds else None
+    # the dominant KERNEL of ours (copy-engine transfers and NCCL's kernels are reported
+    # in roofline.all_kinds but are not our kernels; the push transfer is)
+    ours = [k for k in kinds if k in ("pack", "unpack", "p2p_fused", "ce_reduce")
+            or (k == "ce_copy" and "push" in algos)]
+    dom = max(ours or list(kinds), key=lambda k: kinds[k][2]) if kinds else None
     small = 0   # CE buckets: bytes of the gradients gathered by the pack kernel (< CE_DIRECT_BYTES each)
     for b, x in enumerate(algos):
         if x == "ce":
@@ -613,8 +617,30 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
                     "per_launch": [[k, round(r, 4), round(s, 4), round(e, 4)] for k, r, s, e in tl]
                     if timeline_detail else None}
     ddp.reducer.check_errors()
+    # sanity floor: the last bucket holds the first-registered
+    # params, so its whole sync cannot start before backward ends: exposed >= the
+    # sync time of that bucket alone (same algorithm, measured in isolation)
+    from paper_2006_15704_b200.ddp import GradReducer
+    last = ddp.reducer.bucket_numels()[-1]
+    o2 = dict(opts)
+    o2[L.OPT_ALGO] = L.ddp_bucket_algo(ddp.reducer.ctx, ddp.reducer.num_buckets - 1)
+    solo = GradReducer([last], dtype, last * (4 if dtype == "fp32" else 2), options=o2)
+    gl = torch.empty(last, dtype=torch.float32 if dtype == "fp32" else torch.bfloat16, device=dev)
+    gl.normal_()
+    fl = []
+    for i in range(8):
+        s0, e0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        solo.grad_ready(0, gl, stream)
+        solo.finalize(stream)
+        e0.record(stream)
+        torch.cuda.synchronize(dev)
+        if i >= 3:
+            fl.append(s0.elapsed_time(e0))
+    solo.close()
     vals = [statistics.median(ts), statistics.median(tb), statistics.median(tn) if tn else 0.0]
     vals += [ns_res[n] for n in nosync_every] + [ns_base[n] for n in nosync_every]
+    vals.append(statistics.median(fl))
     vt = torch.tensor(vals, dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vt, op=dist.ReduceOp.MAX)
@@ -624,6 +650,8 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
            "t_bwd_ms": t_bwd, "t_bwd_plus_sync_ms": t_sync, "exposed_ms": t_sync - t_bwd,
            "exposed_pct_of_bwd": 100.0 * (t_sync - t_bwd) / t_bwd,
            "iters": iters, "timing": "median of interleaved passes, max over ranks",
+           "floor_ms": float(vt[-1]),
+           "floor_doc": "whole sync of the last bucket alone (it cannot start before backward ends)",
            "timeline_rank0": timeline if rank == 0 else None}
     if no_overlap:
         res["t_bwd_plus_sync_no_overlap_ms"] = t_noov
