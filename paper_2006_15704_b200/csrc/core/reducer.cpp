@@ -120,6 +120,8 @@ struct ddp_ctx {
   cudaStream_t ce_red = nullptr, ce_pack = nullptr;
   cudaStream_t ce_ag = nullptr, ce_up = nullptr;  // CE2: all-gather copies, unpack
   std::vector<cudaEvent_t> ce_reduced;             // CE2, per bucket: own shard reduced
+  std::vector<cudaStream_t> ce2_rs, ce2_ag;        // CE2: one reduce-scatter / all-gather stream per peer
+  std::vector<cudaEvent_t> ce2_done;               // CE2: joins those streams at finalize
   bool ce2_used = false;
   std::vector<cudaStream_t> ce_cp;          // copy streams: copies of one bucket spread over them
   std::vector<cudaEvent_t> ce_go;           // per bucket: copies may start (comm -> copy streams)
@@ -558,17 +560,19 @@ ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
   CUDA_TRY(c, launch_pack(c->dtype, sv, own, scale, (int)c->pack_ctas, c->ce_pack));
   prof_end(c, c->ce_pack);
   CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
-  CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_packed[b], 0));
-  prof_begin(c, 4);
+  // reduce-scatter: one stream per peer, so the W-1 transfers (and their fixed
+  // latency) overlap on the copy engines; each stream flags its own peer
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
+    cudaStream_t q = c->ce2_rs[i - 1];
+    CUDA_TRY(c, cudaStreamWaitEvent(q, c->ce_packed[b], 0));
+    prof_begin(c, 4, q);
     if (shard_len(j) > 0)
       CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->storage[j]) + bk.ce_off + half + r * bk.ce_stride,
-                                  own + j * L * e, (size_t)(shard_len(j) * e), cudaMemcpyDeviceToDevice, c->comm));
+                                  own + j * L * e, (size_t)(shard_len(j) * e), cudaMemcpyDeviceToDevice, q));
+    prof_end(c, q);
+    if (ddp_status_t st = ce_write(c, q, ce_flag(c, j, 0, b, r), v)) return st;
   }
-  prof_end(c);
-  for (int i = 1; i < W; ++i)
-    if (ddp_status_t st = ce_write(c, c->comm, ce_flag(c, (r + i) % W, 0, b, r), v)) return st;
   // reduce own shard r in rank order
   CUDA_TRY(c, cudaStreamWaitEvent(c->ce_red, c->ce_packed[b], 0));
   for (int i = 1; i < W; ++i)
@@ -581,18 +585,18 @@ ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
   CUDA_TRY(c, launch_shard_reduce(c->dtype, W, src, own + r * L * e, shard_len(r), (int)c->pack_ctas, c->ce_red));
   prof_end(c, c->ce_red);
   CUDA_TRY(c, cudaEventRecord(c->ce_reduced[b], c->ce_red));
-  // all-gather the reduced own shard into every peer's bucket
-  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_ag, c->ce_reduced[b], 0));
-  prof_begin(c, 4, c->ce_ag);
+  // all-gather the reduced own shard into every peer's bucket (one stream per peer)
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
+    cudaStream_t q = c->ce2_ag[i - 1];
+    CUDA_TRY(c, cudaStreamWaitEvent(q, c->ce_reduced[b], 0));
+    prof_begin(c, 4, q);
     if (shard_len(r) > 0)
       CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->storage[j]) + bk.byte_off + r * L * e, own + r * L * e,
-                                  (size_t)(shard_len(r) * e), cudaMemcpyDeviceToDevice, c->ce_ag));
+                                  (size_t)(shard_len(r) * e), cudaMemcpyDeviceToDevice, q));
+    prof_end(c, q);
+    if (ddp_status_t st = ce_write(c, q, ce_flag(c, j, 2, b, r), v)) return st;
   }
-  prof_end(c, c->ce_ag);
-  for (int i = 1; i < W; ++i)
-    if (ddp_status_t st = ce_write(c, c->ce_ag, ce_flag(c, (r + i) % W, 2, b, r), v)) return st;
   // unpack once every shard has arrived
   CUDA_TRY(c, cudaStreamWaitEvent(c->ce_up, c->ce_reduced[b], 0));
   for (int i = 1; i < W; ++i)
@@ -951,6 +955,8 @@ void ddp_destroy(ddp_ctx_t* c) {
   for (cudaEvent_t e : c->prof_ready) cudaEventDestroy(e);
   if (c->comm_done) cudaEventDestroy(c->comm_done);
   std::vector<cudaStream_t> own = c->ce_cp;
+  own.insert(own.end(), c->ce2_rs.begin(), c->ce2_rs.end());
+  own.insert(own.end(), c->ce2_ag.begin(), c->ce2_ag.end());
   own.push_back(c->ce_ag);
   own.push_back(c->ce_up);
   own.push_back(c->ce_red);
@@ -962,6 +968,7 @@ void ddp_destroy(ddp_ctx_t* c) {
   }
   for (cudaEvent_t e : c->ce_go) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ce_reduced) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->ce2_done) cudaEventDestroy(e);
   for (int k = 1; k < kMaxLanes; ++k) {
     if (c->lane_stream[k]) {
       if (!c->poisoned) cudaStreamSynchronize(c->lane_stream[k]);
@@ -1101,6 +1108,12 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
     c->ce_copied.assign(c->buckets.size(), nullptr);
     for (auto& e : c->ce_copied) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_ag, cudaStreamNonBlocking, hi));
+    c->ce2_rs.assign((size_t)(c->world - 1), nullptr);
+    c->ce2_ag.assign((size_t)(c->world - 1), nullptr);
+    for (auto& q : c->ce2_rs) CUDA_TRY(c, cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
+    for (auto& q : c->ce2_ag) CUDA_TRY(c, cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
+    c->ce2_done.assign(2 * (size_t)(c->world - 1), nullptr);
+    for (auto& e : c->ce2_done) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_up, cudaStreamNonBlocking, hi));
     c->ce_reduced.assign(c->buckets.size(), nullptr);
     for (auto& e : c->ce_reduced) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -1220,9 +1233,15 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
         CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_red_done, 0));
         c->ce_used = false;
       }
-      if (c->ce2_used) {  // CE2 writes .grad on the unpack stream
+      if (c->ce2_used) {  // CE2 writes .grad on the unpack stream; its copies read the bucket
         CUDA_TRY(c, cudaEventRecord(c->ce_red_done, c->ce_up));
         CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_red_done, 0));
+        for (size_t k = 0; k < c->ce2_rs.size(); ++k) {
+          CUDA_TRY(c, cudaEventRecord(c->ce2_done[2 * k], c->ce2_rs[k]));
+          CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce2_done[2 * k], 0));
+          CUDA_TRY(c, cudaEventRecord(c->ce2_done[2 * k + 1], c->ce2_ag[k]));
+          CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce2_done[2 * k + 1], 0));
+        }
         c->ce2_used = false;
       }
       for (size_t k = 1; k < c->rr_stream.size(); ++k) {
