@@ -560,11 +560,10 @@ ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
   CUDA_TRY(c, launch_pack(c->dtype, sv, own, scale, (int)c->pack_ctas, c->ce_pack));
   prof_end(c, c->ce_pack);
   CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
-  // reduce-scatter: one stream per peer, so the W-1 transfers (and their fixed
-  // latency) overlap on the copy engines; each stream flags its own peer
+  // reduce-scatter on the CE2 copy stream(s); each transfer is followed by its peer's flag
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
-    cudaStream_t q = c->ce2_rs[i - 1];
+    cudaStream_t q = c->ce2_rs[(i - 1) % c->ce2_rs.size()];
     CUDA_TRY(c, cudaStreamWaitEvent(q, c->ce_packed[b], 0));
     prof_begin(c, 4, q);
     if (shard_len(j) > 0)
@@ -585,10 +584,10 @@ ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
   CUDA_TRY(c, launch_shard_reduce(c->dtype, W, src, own + r * L * e, shard_len(r), (int)c->pack_ctas, c->ce_red));
   prof_end(c, c->ce_red);
   CUDA_TRY(c, cudaEventRecord(c->ce_reduced[b], c->ce_red));
-  // all-gather the reduced own shard into every peer's bucket (one stream per peer)
+  // all-gather the reduced own shard into every peer's bucket
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
-    cudaStream_t q = c->ce2_ag[i - 1];
+    cudaStream_t q = c->ce2_ag[(i - 1) % c->ce2_ag.size()];
     CUDA_TRY(c, cudaStreamWaitEvent(q, c->ce_reduced[b], 0));
     prof_begin(c, 4, q);
     if (shard_len(r) > 0)
@@ -1108,11 +1107,15 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
     c->ce_copied.assign(c->buckets.size(), nullptr);
     for (auto& e : c->ce_copied) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_ag, cudaStreamNonBlocking, hi));
-    c->ce2_rs.assign((size_t)(c->world - 1), nullptr);
-    c->ce2_ag.assign((size_t)(c->world - 1), nullptr);
+    // CE2 copy streams: CE_STREAMS of them (peers round-robin).  One per peer was
+    // measured slower at W=4 (profiles/r01_n4.md): the copy engines do not overlap
+    // transfers usefully, the extra streams only add ordering hops
+    const size_t nst = (size_t)std::max<int64_t>(1, std::min<int64_t>(c->ce_streams, c->world - 1));
+    c->ce2_rs.assign(nst, nullptr);
+    c->ce2_ag.assign(nst, nullptr);
     for (auto& q : c->ce2_rs) CUDA_TRY(c, cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
     for (auto& q : c->ce2_ag) CUDA_TRY(c, cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
-    c->ce2_done.assign(2 * (size_t)(c->world - 1), nullptr);
+    c->ce2_done.assign(2 * nst, nullptr);
     for (auto& e : c->ce2_done) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_up, cudaStreamNonBlocking, hi));
     c->ce_reduced.assign(c->buckets.size(), nullptr);
