@@ -93,6 +93,35 @@ int main(int argc, char** argv) {
     CK(cudaEventElapsedTime(&ms, e0, e1));
     printf("copy-engine peer 0->1 %zu MiB: %.1f GB/s\n", bytes >> 20, bytes / (ms / reps * 1e-3) / 1e9);
   }
+  // copy engines in both directions at once (what a 2-rank copy-engine exchange does),
+  // one 256 MiB transfer and 25 MiB transfers (bucket-sized), timed on each device
+  for (size_t chunk : {bytes, (size_t)25 << 20}) {
+    cudaStream_t s[2];
+    cudaEvent_t ev[2][2];
+    for (int d = 0; d < 2; ++d) {
+      CK(cudaSetDevice(d));
+      CK(cudaStreamCreate(&s[d]));
+      CK(cudaEventCreate(&ev[d][0]));
+      CK(cudaEventCreate(&ev[d][1]));
+    }
+    const int nrep = (int)(bytes / chunk) * reps;
+    for (int d = 0; d < 2; ++d) {
+      CK(cudaSetDevice(d));
+      CK(cudaEventRecord(ev[d][0], s[d]));
+      for (int r = 0; r < nrep; ++r)
+        CK(d == 0 ? cudaMemcpyPeerAsync(b1, 1, a0, 0, chunk, s[0]) : cudaMemcpyPeerAsync(b0, 0, a1, 1, chunk, s[1]));
+      CK(cudaEventRecord(ev[d][1], s[d]));
+    }
+    for (int d = 0; d < 2; ++d) {
+      CK(cudaSetDevice(d));
+      CK(cudaEventSynchronize(ev[d][1]));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, ev[d][0], ev[d][1]));
+      printf("copy-engine bidirectional %zu MiB transfers: gpu%d -> peer %.1f GB/s per direction\n", chunk >> 20, d,
+             (double)chunk * nrep / (ms * 1e-3) / 1e9);
+    }
+  }
+  CK(cudaSetDevice(0));
   const int ctas_list[] = {8, 16, 32, 64, 96, 128, 148, 296};
   kfn fns[] = {copy_kernel<1>, copy_kernel<4>, copy_kernel<8>};
   const int us[] = {1, 4, 8};
