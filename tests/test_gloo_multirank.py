@@ -78,3 +78,64 @@ def test_two_ranks_agree_on_launch_order_and_nccl_id():
             assert seq == list(range(nb))         # 0,1,2,... on every rank, every pass
     ids = res[0][2]
     assert ids[0] == ids[1] == res[0][3] and len(ids[0]) == 128
+
+
+def _worker_unused(rank, world, port, q):
+    """Each rank: rank-specific unused sets (marked at 'forward end', Alg. 1
+    L224-L225) and rank-specific hook orders, traced order-rebuilt maps (rank
+    0's order broadcast through the process group, as the front end does)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2006_15704_b200 import _lib as L
+        from synth.shapes import numels
+        ns = numels("resnet50")
+        rng = random.Random(7 + rank)
+        ctx = L.ddp_create(ns, L.FP32, 5 << 20, world, rank)
+        L.ddp_set_option(ctx, L.OPT_DRY_RUN, 1)
+        L.ddp_set_option(ctx, L.OPT_FIND_UNUSED, 1)
+        seqs = []
+        for _ in range(4):
+            unused = set(rng.sample(range(len(ns)), 20))
+            for p in sorted(unused):
+                L.ddp_mark_unused(ctx, p, 0, 0)
+            order = [p for p in range(len(ns)) if p not in unused]
+            rng.shuffle(order)
+            for p in order:
+                L.ddp_grad_ready(ctx, p, 0, 0)
+            L.ddp_finalize_backward(ctx, 0)
+            seqs.append([b for b, _ in L.ddp_launch_trace(ctx)])
+        traced = L.ddp_ready_order(ctx)
+        L.ddp_destroy(ctx)
+        t = torch.tensor(traced, dtype=torch.int32)
+        dist.broadcast(t, src=0)                     # the agreed order (rank 0's)
+        c2 = L.ddp_create_ordered(ns, t.tolist(), L.FP32, 5 << 20, world, rank)
+        mapping = [(L.ddp_bucket_info(c2, b)[0],
+                    [L.ddp_bucket_slot(c2, b, s) for s in range(L.ddp_bucket_info(c2, b)[1])])
+                   for b in range(L.ddp_num_buckets(c2))]
+        L.ddp_destroy(c2)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, (seqs, mapping))
+        q.put((rank, gathered))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_unused_and_rebuilt_map_agree():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_unused, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    gathered = res[0][1]
+    (s0, m0), (s1, m1) = gathered
+    nb = len(s0[0])
+    assert all(seq == list(range(nb)) for seq in s0 + s1)   # same launch sequence on both ranks
+    assert m0 == m1                                           # same rebuilt map on both ranks
