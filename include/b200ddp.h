@@ -86,8 +86,9 @@ enum {
   DDP_OPT_MULTICAST = 11,       /* 1: the caller will pass a multicast (NVLS) address of the storage
                                    to ddp_bind_device, enabling DDP_ALGO_NVLS; CREATED only.  Every
                                    rank must agree.  Never increases ddp_storage_bytes */
-  DDP_OPT_CE_STREAMS = 12,      /* copy-engine algorithm: number of streams its peer copies are
-                                   spread over (1..16, default 1 = the comm stream); before binding */
+  DDP_OPT_CE_STREAMS = 12,      /* CE2: number of streams its peer copies are spread over (1..16,
+                                   default 1; more measured slower).  CE copies use the comm stream.
+                                   Before binding */
   DDP_OPT_NCCL_COMMS = 13,      /* round-robin process groups (Fig. 12 "rrx"): NCCL
                                    bucket b runs on communicator b mod k (split off the first with
                                    ncclCommSplit) and its own stream; 1..8, default 1; before binding */

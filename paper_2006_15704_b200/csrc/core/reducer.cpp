@@ -123,9 +123,6 @@ struct ddp_ctx {
   std::vector<cudaStream_t> ce2_rs, ce2_ag;        // CE2: one reduce-scatter / all-gather stream per peer
   std::vector<cudaEvent_t> ce2_done;               // CE2: joins those streams at finalize
   bool ce2_used = false;
-  std::vector<cudaStream_t> ce_cp;          // copy streams: copies of one bucket spread over them
-  std::vector<cudaEvent_t> ce_go;           // per bucket: copies may start (comm -> copy streams)
-  std::vector<cudaEvent_t> ce_cp_done;      // per bucket x copy stream: its copies issued
   std::vector<cudaEvent_t> ce_packed;  // per bucket: small gradients gathered (pack -> comm stream)
   std::vector<cudaEvent_t> ce_copied;  // per bucket: copies issued (comm -> reduce stream)
   std::vector<void*> ce_grad;          // scratch argument arrays
@@ -443,12 +440,12 @@ ddp_status_t launch_ce(ddp_ctx* c, int b) {
     else CUDA_TRY(c, launch_ce_gather(c->dtype, gv, own_slot, (int)c->pack_ctas, c->ce_pack));
     prof_end(c, c->ce_pack);
     CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
-    CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_packed[b], 0));
   }
   // reuse guard: every peer has consumed (reduced) its slot r of this bucket from pass v-1
   if (v > 1)
     for (int i = 1; i < W; ++i)
       if (ddp_status_t st = ce_wait(c, c->comm, ce_flag(c, r, 1, b, (r + i) % W), v - 1)) return st;
+  prof_begin(c, 4);
   if (push) {  // SM push: one kernel reads each gradient once and stores it into every peer
     void* peers[kMaxWorld];
     for (int i = 1; i < W; ++i)
@@ -457,53 +454,29 @@ ddp_status_t launch_ce(ddp_ctx* c, int b) {
     c->ce_wire.assign(bk.ce_wire.begin(), bk.ce_wire.end());
     for (size_t k = 0; k < ns; ++k) c->ce_numel.push_back(bk.off[k + 1] - bk.off[k]);
     const CeView pv{c->ce_grad.data(), c->ce_wire.data(), c->ce_numel.data(), (int32_t)ns};
-    prof_begin(c, 4);
     CUDA_TRY(c, launch_ce_push(c->dtype, pv, peers, W - 1, (int)std::min<int64_t>(c->comm_ctas, 148), c->comm));
-    prof_end(c);
-  }
-  // Copies spread over the copy streams (each transfer carries a few us of fixed
-  // latency; independent streams let several copy engines overlap it), the
-  // largest-first into the least loaded stream.
-  const int K = push ? 0 : (int)c->ce_cp.size();
-  if (!push) prof_begin(c, 4);
-  if (K > 1) CUDA_TRY(c, cudaEventRecord(c->ce_go[b], c->comm));
-  int64_t load[16] = {};
-  bool used[16] = {};
-  auto issue = [&](void* dst, const void* src, int64_t bytes) -> ddp_status_t {
-    if (K == 1) {  // one copy stream: the comm stream itself (no event hops)
-      CUDA_TRY(c, cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, c->comm));
-      return DDP_OK;
+  } else {
+    // copy engines: the large gradients straight from .grad first (they do not wait
+    // for the gather), then the gathered region of the small ones
+    for (int i = 1; i < W; ++i) {
+      char* dst = static_cast<char*>(c->storage[(r + i) % W]) + bk.ce_off + r * bk.ce_stride;
+      for (size_t k = 0; k < ns; ++k)
+        if (bk.ce_direct[k])
+          CUDA_TRY(c, cudaMemcpyAsync(dst + bk.ce_wire[k] * c->esize, bk.grads[k],
+                                      (size_t)((bk.off[k + 1] - bk.off[k]) * c->esize), cudaMemcpyDeviceToDevice,
+                                      c->comm));
     }
-    int best = 0;
-    for (int q = 1; q < K; ++q)
-      if (load[q] < load[best]) best = q;
-    if (!used[best]) {
-      CUDA_TRY(c, cudaStreamWaitEvent(c->ce_cp[best], c->ce_go[b], 0));
-      used[best] = true;
+    if (any_small) {
+      CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_packed[b], 0));
+      for (int i = 1; i < W; ++i) {
+        char* dst = static_cast<char*>(c->storage[(r + i) % W]) + bk.ce_off + r * bk.ce_stride;
+        CUDA_TRY(c, cudaMemcpyAsync(dst + bk.ce_small0 * we, own_slot + bk.ce_small0 * we,
+                                    (size_t)((bk.ce_wire_numel - bk.ce_small0) * we), cudaMemcpyDeviceToDevice,
+                                    c->comm));
+      }
     }
-    load[best] += bytes + (1 << 20);  // + fixed cost of a transfer, in bytes
-    CUDA_TRY(c, cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice, c->ce_cp[best]));
-    return DDP_OK;
-  };
-  for (int i = 1; i < W; ++i) {
-    const int j = (r + i) % W;
-    char* dst = static_cast<char*>(c->storage[j]) + bk.ce_off + r * bk.ce_stride;
-    for (size_t k = 0; k < ns; ++k)
-      if (bk.ce_direct[k])
-        if (ddp_status_t st = issue(dst + bk.ce_wire[k] * c->esize, bk.grads[k], (bk.off[k + 1] - bk.off[k]) * c->esize))
-          return st;
-    if (any_small)
-      if (ddp_status_t st = issue(dst + bk.ce_small0 * we, own_slot + bk.ce_small0 * we,
-                                  (bk.ce_wire_numel - bk.ce_small0) * we))
-        return st;
   }
-  for (int q = 0; q < K && K > 1; ++q) {
-    if (!used[q]) continue;
-    cudaEvent_t e = c->ce_cp_done[(size_t)b * K + q];
-    CUDA_TRY(c, cudaEventRecord(e, c->ce_cp[q]));
-    CUDA_TRY(c, cudaStreamWaitEvent(c->comm, e, 0));
-  }
-  if (!push) prof_end(c);
+  prof_end(c);
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
     if (ddp_status_t st = ce_write(c, c->comm, ce_flag(c, j, 0, b, r), v)) return st;
@@ -743,7 +716,7 @@ ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
     for (size_t k = 1; k < c->rr_stream.size(); ++k) CUDA_TRY(c, cudaStreamWaitEvent(c->rr_stream[k], ev, 0));
     for (int k = 1; k < kMaxLanes; ++k)
       if (c->lane_stream[k]) CUDA_TRY(c, cudaStreamWaitEvent(c->lane_stream[k], ev, 0));
-    for (cudaStream_t q : c->ce_cp) CUDA_TRY(c, cudaStreamWaitEvent(q, ev, 0));
+    for (cudaStream_t q : c->ce2_rs) CUDA_TRY(c, cudaStreamWaitEvent(q, ev, 0));
   }
   c->unwaited.clear();
   if (c->world == 1 && !c->emulated) {
@@ -953,8 +926,7 @@ void ddp_destroy(ddp_ctx_t* c) {
   for (cudaEvent_t e : c->event_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : c->prof_ready) cudaEventDestroy(e);
   if (c->comm_done) cudaEventDestroy(c->comm_done);
-  std::vector<cudaStream_t> own = c->ce_cp;
-  own.insert(own.end(), c->ce2_rs.begin(), c->ce2_rs.end());
+  std::vector<cudaStream_t> own(c->ce2_rs.begin(), c->ce2_rs.end());
   own.insert(own.end(), c->ce2_ag.begin(), c->ce2_ag.end());
   own.push_back(c->ce_ag);
   own.push_back(c->ce_up);
@@ -965,7 +937,6 @@ void ddp_destroy(ddp_ctx_t* c) {
     if (!c->poisoned) cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
   }
-  for (cudaEvent_t e : c->ce_go) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ce_reduced) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ce2_done) cudaEventDestroy(e);
   for (int k = 1; k < kMaxLanes; ++k) {
@@ -975,7 +946,6 @@ void ddp_destroy(ddp_ctx_t* c) {
     }
     if (c->lane_done[k]) cudaEventDestroy(c->lane_done[k]);
   }
-  for (cudaEvent_t e : c->ce_cp_done) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ce_packed) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ce_copied) cudaEventDestroy(e);
   if (c->ce_red_done) cudaEventDestroy(c->ce_red_done);
@@ -1120,12 +1090,7 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_up, cudaStreamNonBlocking, hi));
     c->ce_reduced.assign(c->buckets.size(), nullptr);
     for (auto& e : c->ce_reduced) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    c->ce_cp.assign((size_t)c->ce_streams, nullptr);
-    for (auto& q : c->ce_cp) CUDA_TRY(c, cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
-    c->ce_go.assign(c->buckets.size(), nullptr);
-    for (auto& e : c->ce_go) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    c->ce_cp_done.assign(c->buckets.size() * (size_t)c->ce_streams, nullptr);
-    for (auto& e : c->ce_cp_done) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->ce_red_done, cudaEventDisableTiming));
     cudaDriverEntryPointQueryResult q1, q2;
     CUDA_TRY(c, cudaGetDriverEntryPoint("cuStreamWriteValue32", &c->fn_write32, cudaEnableDefault, &q1));
