@@ -1,0 +1,410 @@
+// exchange.cpp — device side of the host core: what a launched bucket does
+// (Alg. 1: pack into the bucket, AllReduce, copy back),
+// per algorithm, on the comm stream / lanes / copy-engine
+// streams after the producer streams (overlap), and the
+// find_unused bitmap step.  Called from core/reducer.cpp.
+#include <algorithm>
+#include <cstring>
+
+#include "ctx.h"
+
+namespace b200ddp {
+
+// ---- profiling -------------------------------------------------------------
+cudaEvent_t pool_event(ddp_ctx* c) {
+  if (!c->event_pool.empty()) {
+    cudaEvent_t e = c->event_pool.back();
+    c->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+void prof_begin(ddp_ctx* c, int kind, cudaStream_t s) {
+  if (!c->profile) return;
+  ProfRec r{kind, pool_event(c), pool_event(c), (int)c->prof_ready.size() - 1};
+  cudaEventRecord(r.a, s ? s : c->comm);
+  c->prof.push_back(r);
+}
+void prof_end(ddp_ctx* c, cudaStream_t s) {
+  if (!c->profile || c->prof.empty()) return;
+  cudaEventRecord(c->prof.back().b, s ? s : c->comm);
+}
+
+typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+
+// ce flags of bucket b in a rank's storage: [0][b][src] ready, [1][b][src] consumed
+uint32_t* ce_flag(const ddp_ctx* c, int r, int kind, int b, int src) {
+  return reinterpret_cast<uint32_t*>(static_cast<char*>(c->storage[r]) + c->ce_flags_off) +
+         ((size_t)kind * c->buckets.size() + b) * kMaxWorld + src;
+}
+
+ddp_status_t ce_write(ddp_ctx* c, cudaStream_t s, uint32_t* addr, uint32_t v) {
+  // default flags: a memory fence precedes the write (stream-scoped __threadfence_system)
+  CUresult r = reinterpret_cast<StreamValueFn>(c->fn_write32)((CUstream)s, (CUdeviceptr)addr, v, 0);
+  if (r != CUDA_SUCCESS) return cuda_fail(c, cudaErrorUnknown, "cuStreamWriteValue32");
+  return DDP_OK;
+}
+ddp_status_t ce_wait(ddp_ctx* c, cudaStream_t s, uint32_t* addr, uint32_t v) {
+  CUresult r = reinterpret_cast<StreamValueFn>(c->fn_wait32)((CUstream)s, (CUdeviceptr)addr, v,
+                                                              CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return cuda_fail(c, cudaErrorUnknown, "cuStreamWaitValue32");
+  return DDP_OK;
+}
+
+// Copy-engine one-shot (SM-free exchange).  Rank r's raw gradients go to slot r
+// of every peer: large ones by one cudaMemcpyAsync each straight from .grad,
+// the small ones gathered (kernel) into r's own slot and sent as one region.
+// Stream memory operations order everything, so no SM spins while waiting:
+//   comm stream:    [wait: peers consumed pass v-1] -> copies -> ready flags to peers
+//   reduce stream:  [wait: own copies issued, peers' ready flags] -> rank-order
+//                   reduce x 1/W per operand straight into .grad -> consumed flags
+ddp_status_t launch_ce(ddp_ctx* c, int b) {
+  Bucket& bk = c->buckets[b];
+  const int W = c->world, r = c->rank;
+  char* mine = static_cast<char*>(c->storage[r]);
+  char* own_slot = mine + bk.ce_off + r * bk.ce_stride;
+  const uint32_t v = ++bk.ce_count;
+  const size_t ns = bk.params.size();
+  const bool push = bk.algo == DDP_ALGO_PUSH;
+  c->ce_grad.clear();
+  c->ce_wire.clear();
+  c->ce_numel.clear();
+  for (size_t k = 0; k < ns && !push; ++k) {
+    if (bk.ce_direct[k]) continue;
+    c->ce_grad.push_back(bk.grads[k]);
+    c->ce_wire.push_back(bk.ce_wire[k]);
+    c->ce_numel.push_back(bk.off[k + 1] - bk.off[k]);
+  }
+  const bool any_small = !c->ce_grad.empty();
+  const int64_t we = c->wire_bf16 ? 2 : c->esize;  // wire element bytes
+  const float scale = 1.0f / (float)W;
+  if (any_small) {  // gather on its own stream so it overlaps the previous bucket's copies
+    const CeView gv{c->ce_grad.data(), c->ce_wire.data(), c->ce_numel.data(), (int32_t)c->ce_grad.size()};
+    prof_begin(c, 0, c->ce_pack);
+    if (c->wire_bf16) CUDA_TRY(c, launch_wire_gather(gv, own_slot, scale, (int)c->pack_ctas, c->ce_pack));
+    else CUDA_TRY(c, launch_ce_gather(c->dtype, gv, own_slot, (int)c->pack_ctas, c->ce_pack));
+    prof_end(c, c->ce_pack);
+    CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
+  }
+  // reuse guard: every peer has consumed (reduced) its slot r of this bucket from pass v-1
+  if (v > 1)
+    for (int i = 1; i < W; ++i)
+      if (ddp_status_t st = ce_wait(c, c->comm, ce_flag(c, r, 1, b, (r + i) % W), v - 1)) return st;
+  prof_begin(c, 4);
+  if (push) {  // SM push: one kernel reads each gradient once and stores it into every peer
+    void* peers[kMaxWorld];
+    for (int i = 1; i < W; ++i)
+      peers[i - 1] = static_cast<char*>(c->storage[(r + i) % W]) + bk.ce_off + r * bk.ce_stride;
+    c->ce_grad.assign(bk.grads.begin(), bk.grads.end());
+    c->ce_wire.assign(bk.ce_wire.begin(), bk.ce_wire.end());
+    for (size_t k = 0; k < ns; ++k) c->ce_numel.push_back(bk.off[k + 1] - bk.off[k]);
+    const CeView pv{c->ce_grad.data(), c->ce_wire.data(), c->ce_numel.data(), (int32_t)ns};
+    CUDA_TRY(c, launch_ce_push(c->dtype, pv, peers, W - 1, (int)std::min<int64_t>(c->comm_ctas, 148), c->comm));
+  } else {
+    // copy engines: the large gradients straight from .grad first (they do not wait
+    // for the gather), then the gathered region of the small ones
+    for (int i = 1; i < W; ++i) {
+      char* dst = static_cast<char*>(c->storage[(r + i) % W]) + bk.ce_off + r * bk.ce_stride;
+      for (size_t k = 0; k < ns; ++k)
+        if (bk.ce_direct[k])
+          CUDA_TRY(c, cudaMemcpyAsync(dst + bk.ce_wire[k] * c->esize, bk.grads[k],
+                                      (size_t)((bk.off[k + 1] - bk.off[k]) * c->esize), cudaMemcpyDeviceToDevice,
+                                      c->comm));
+    }
+    if (any_small) {
+      CUDA_TRY(c, cudaStreamWaitEvent(c->comm, c->ce_packed[b], 0));
+      for (int i = 1; i < W; ++i) {
+        char* dst = static_cast<char*>(c->storage[(r + i) % W]) + bk.ce_off + r * bk.ce_stride;
+        CUDA_TRY(c, cudaMemcpyAsync(dst + bk.ce_small0 * we, own_slot + bk.ce_small0 * we,
+                                    (size_t)((bk.ce_wire_numel - bk.ce_small0) * we), cudaMemcpyDeviceToDevice,
+                                    c->comm));
+      }
+    }
+  }
+  prof_end(c);
+  for (int i = 1; i < W; ++i) {
+    const int j = (r + i) % W;
+    if (ddp_status_t st = ce_write(c, c->comm, ce_flag(c, j, 0, b, r), v)) return st;
+  }
+  // the reduction overwrites .grad, which the copies above read: order after them
+  CUDA_TRY(c, cudaEventRecord(c->ce_copied[b], c->comm));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_red, c->ce_copied[b], 0));
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_wait(c, c->ce_red, ce_flag(c, r, 0, b, (r + i) % W), v)) return st;
+  c->ce_grad.assign(bk.grads.begin(), bk.grads.end());
+  c->ce_wire.assign(bk.ce_wire.begin(), bk.ce_wire.end());
+  c->ce_numel.clear();
+  for (size_t k = 0; k < ns; ++k) c->ce_numel.push_back(bk.off[k + 1] - bk.off[k]);
+  const CeView rv{c->ce_grad.data(), c->ce_wire.data(), c->ce_numel.data(), (int32_t)ns};
+  prof_begin(c, 5, c->ce_red);
+  if (c->wire_bf16)
+    CUDA_TRY(c, launch_wire_reduce(W, r, rv, mine + bk.ce_off, bk.ce_stride, scale, (int)c->pack_ctas, c->ce_red));
+  else
+    CUDA_TRY(c, launch_ce_reduce(c->dtype, W, r, rv, mine + bk.ce_off, bk.ce_stride, scale, (int)c->pack_ctas,
+                                 c->ce_red));
+  prof_end(c, c->ce_red);
+  for (int i = 1; i < W; ++i) {
+    const int j = (r + i) % W;
+    if (ddp_status_t st = ce_write(c, c->ce_red, ce_flag(c, j, 1, b, r), v)) return st;
+  }
+  c->ce_used = true;
+  return DDP_OK;
+}
+
+// Copy-engine two-shot (CE2): the reduce-scatter and all-gather of a ring /
+// two-shot, 2 (W-1)/W S NVLink bytes per direction, moved by copy engines and
+// ordered by stream memory operations (no SM waits):
+//   pack stream:    pack x 1/W into the own bucket
+//   comm stream:    shard j of the own bucket -> peer j's staging slot r (half v%2);
+//                   ready flags
+//   reduce stream:  [wait all ready] own shard = rank-order sum of the W values
+//                   (slot q, own bucket for q = r), in place in the own bucket
+//   all-gather:     [after the reduce] own shard -> shard r of every peer's bucket;
+//                   gathered flags
+//   unpack stream:  [wait all gathered] own bucket -> .grad
+// Staging is double-buffered by pass parity, so no "consumed" flags are needed:
+// writing half v%2 again (pass v+2) follows, through this rank's own finalize,
+// every peer's all-gather of pass v+1, which follows its reduce of pass v.
+ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
+  Bucket& bk = c->buckets[b];
+  const int W = c->world, r = c->rank;
+  const uint32_t v = ++bk.ce_count;
+  char* mine = static_cast<char*>(c->storage[r]);
+  char* own = mine + bk.byte_off;
+  const int64_t L = bk.shard, e = c->esize;
+  const int64_t half = (int64_t)(v & 1) * W * bk.ce_stride;
+  auto shard_len = [&](int j) { return std::max<int64_t>(0, std::min<int64_t>(L, bk.numel - j * L)); };
+  prof_begin(c, 0, c->ce_pack);
+  CUDA_TRY(c, launch_pack(c->dtype, sv, own, scale, (int)c->pack_ctas, c->ce_pack));
+  prof_end(c, c->ce_pack);
+  CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
+  // reduce-scatter on the CE2 copy stream(s); each transfer is followed by its peer's flag
+  for (int i = 1; i < W; ++i) {
+    const int j = (r + i) % W;
+    cudaStream_t q = c->ce2_rs[(i - 1) % c->ce2_rs.size()];
+    CUDA_TRY(c, cudaStreamWaitEvent(q, c->ce_packed[b], 0));
+    prof_begin(c, 4, q);
+    if (shard_len(j) > 0)
+      CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->storage[j]) + bk.ce_off + half + r * bk.ce_stride,
+                                  own + j * L * e, (size_t)(shard_len(j) * e), cudaMemcpyDeviceToDevice, q));
+    prof_end(c, q);
+    if (ddp_status_t st = ce_write(c, q, ce_flag(c, j, 0, b, r), v)) return st;
+  }
+  // reduce own shard r in rank order
+  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_red, c->ce_packed[b], 0));
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_wait(c, c->ce_red, ce_flag(c, r, 0, b, (r + i) % W), v)) return st;
+  const void* src[kMaxWorld];
+  for (int q = 0; q < W; ++q)
+    src[q] = q == r ? static_cast<const void*>(own + r * L * e)
+                    : static_cast<const void*>(mine + bk.ce_off + half + q * bk.ce_stride);
+  prof_begin(c, 5, c->ce_red);
+  CUDA_TRY(c, launch_shard_reduce(c->dtype, W, src, own + r * L * e, shard_len(r), (int)c->pack_ctas, c->ce_red));
+  prof_end(c, c->ce_red);
+  CUDA_TRY(c, cudaEventRecord(c->ce_reduced[b], c->ce_red));
+  // all-gather the reduced own shard into every peer's bucket
+  for (int i = 1; i < W; ++i) {
+    const int j = (r + i) % W;
+    cudaStream_t q = c->ce2_ag[(i - 1) % c->ce2_ag.size()];
+    CUDA_TRY(c, cudaStreamWaitEvent(q, c->ce_reduced[b], 0));
+    prof_begin(c, 4, q);
+    if (shard_len(r) > 0)
+      CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->storage[j]) + bk.byte_off + r * L * e, own + r * L * e,
+                                  (size_t)(shard_len(r) * e), cudaMemcpyDeviceToDevice, q));
+    prof_end(c, q);
+    if (ddp_status_t st = ce_write(c, q, ce_flag(c, j, 2, b, r), v)) return st;
+  }
+  // unpack once every shard has arrived
+  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_up, c->ce_reduced[b], 0));
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_wait(c, c->ce_up, ce_flag(c, r, 2, b, (r + i) % W), v)) return st;
+  prof_begin(c, 2, c->ce_up);
+  CUDA_TRY(c, launch_unpack(c->dtype, sv, own, (int)c->pack_ctas, c->ce_up));
+  prof_end(c, c->ce_up);
+  c->ce2_used = true;
+  return DDP_OK;
+}
+
+// ---- a3/a4/a6 device work for one bucket -------------------------------------
+ddp_status_t launch_device(ddp_ctx* c, int b) {
+  Bucket& bk = c->buckets[b];
+  const SlotView sv{bk.off.data(), bk.grads.data(), (int32_t)bk.params.size()};
+  const float scale = 1.0f / (float)c->world;  // fl(1/W), reading C-2
+  char* mine = static_cast<char*>(c->storage[c->rank]);
+  if (bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH) return launch_ce(c, b);
+  if (bk.algo == DDP_ALGO_CE2) return launch_ce2(c, b, sv, scale);
+  if (bk.algo == DDP_ALGO_NCCL) {
+    void* buf = mine + bk.byte_off;
+    const size_t k = c->rr_comm.empty() ? 0 : (size_t)b % c->rr_comm.size();
+    cudaStream_t s = k == 0 ? c->comm : c->rr_stream[k];
+    ncclComm_t comm = k == 0 ? c->nccl : c->rr_comm[k];
+    if (k) c->rr_used[k] = 1;
+    prof_begin(c, 0, s);
+    CUDA_TRY(c, launch_pack(c->dtype, sv, buf, scale, (int)c->pack_ctas, s));
+    prof_end(c, s);
+    prof_begin(c, 1, s);
+    NCCL_TRY(c, ncclAllReduce(buf, buf, (size_t)bk.numel, c->dtype == DDP_FP32 ? ncclFloat32 : ncclBfloat16,
+                              ncclSum, comm, s));
+    prof_end(c, s);
+    prof_begin(c, 2, s);
+    CUDA_TRY(c, launch_unpack(c->dtype, sv, buf, (int)c->pack_ctas, s));
+    prof_end(c, s);
+    return DDP_OK;
+  }
+  // lane: its stream, flag table, sequence and staging (identical choice on every rank)
+  // Lanes run spinning kernels side by side: all of them must fit on the SMs at
+  // once (one CTA per SM guaranteed), else a lane could wait for a peer lane that
+  // cannot be scheduled.  Same options on every rank -> same choice everywhere.
+  const int nl = c->lanes * std::min<int64_t>(c->comm_ctas, kMaxCtas) <= 148 ? (int)c->lanes : 1;
+  const int ln = (c->emulated || c->world == 1) ? 0 : b % nl;
+  cudaStream_t ls = ln == 0 ? c->comm : c->lane_stream[ln];
+  if (ln) c->lane_used[ln] = true;
+  P2PLaunch a{};
+  for (int r = 0; r < c->world; ++r) a.storage[r] = c->storage[r];
+  a.flags_byte_off = c->flags_off + ln * kFlagsBytes;
+  a.bucket_byte_off = bk.byte_off;
+  if (bk.algo == DDP_ALGO_TWOSHOT) {
+    a.stage_byte_off = c->stage2_off + ln * c->world * c->stage2_stride;
+    a.stage_stride = c->stage2_stride;
+  } else if (c->world == 1) {
+    a.stage_byte_off = bk.byte_off;  // world 1 packs straight into the bucket
+    a.stage_stride = 0;
+  } else {
+    a.stage_byte_off = c->stage1_off + (int64_t)(2 * ln + (c->p2p_launches[ln] & 1)) * c->world * c->stage1_stride;
+    a.stage_stride = c->stage1_stride;
+  }
+  a.numel = bk.numel;
+  a.shard = bk.shard;
+  a.chunk = bk.chunk;
+  a.world = c->world;
+  a.rank = c->rank;
+  a.ctas = bk.ctas;
+  a.emulated = c->emulated ? 1 : 0;
+  a.sub = bk.sub;
+  a.stages = bk.stages;
+  a.seq = c->p2p_seq[ln];
+  a.scale = scale;
+  a.grad_rank_stride = c->grad_rank_stride;
+  a.err = c->err_dev;
+  a.mc = c->mc;
+  c->p2p_seq[ln] += (uint32_t)bk.stages + 2;  // flag values used: seq .. seq + stages + 1
+  c->p2p_launches[ln] += 1;
+  prof_begin(c, 3, ls);
+  if (bk.algo == DDP_ALGO_NVLS) CUDA_TRY(c, launch_nvls(c->dtype, sv, a, ls));
+  else CUDA_TRY(c, launch_p2p(bk.algo, c->dtype, sv, a, ls));
+  prof_end(c, ls);
+  return DDP_OK;
+}
+
+// World 1: buckets [b0, b1) launched by one call run as ONE fused kernel over
+// the concatenation of their slots (pack into each bucket, 1-rank reduce and
+// unpack from registers); the values equal per-bucket launches bit for bit.
+ddp_status_t launch_local_group(ddp_ctx* c, int b0, int b1) {
+  c->g_off.clear();
+  c->g_grad.clear();
+  c->g_dst.clear();
+  int64_t base = 0;
+  for (int b = b0; b < b1; ++b) {
+    const Bucket& bk = c->buckets[b];
+    for (size_t s = 0; s < bk.params.size(); ++s) {
+      c->g_off.push_back(base + bk.off[s]);
+      c->g_grad.push_back(bk.grads[s]);
+      c->g_dst.push_back(bk.byte_off + bk.off[s] * c->esize);
+    }
+    base += bk.numel;
+  }
+  c->g_off.push_back(base);
+  const GroupView gv{c->g_off.data(), c->g_grad.data(), c->g_dst.data(), (int32_t)c->g_grad.size()};
+  prof_begin(c, 3);
+  CUDA_TRY(c, launch_local(c->dtype, gv, c->storage[c->rank], (int)c->pack_ctas, c->comm));
+  prof_end(c);
+  return DDP_OK;
+}
+
+ddp_status_t device_range(ddp_ctx* c, int b0, int b1);
+
+ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
+  if (b0 >= b1) return DDP_OK;
+  if (c->profile) {  // when the producer reached this launch point (timeline "ready")
+    cudaEvent_t ev = pool_event(c);
+    CUDA_TRY(c, cudaEventRecord(ev, c->unwaited.empty() ? c->comm : c->unwaited.front()));
+    c->prof_ready.push_back(ev);
+  }
+  // comm stream waits for everything the producers enqueued so far
+  for (cudaStream_t s : c->unwaited) {
+    cudaEvent_t ev = nullptr;
+    for (auto& se : c->stream_events)
+      if (se.first == s) ev = se.second;
+    if (!ev) {
+      CUDA_TRY(c, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      c->stream_events.emplace_back(s, ev);
+    }
+    CUDA_TRY(c, cudaEventRecord(ev, s));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->comm, ev, 0));
+    if (c->ce_pack) CUDA_TRY(c, cudaStreamWaitEvent(c->ce_pack, ev, 0));
+    if (c->ce_up) CUDA_TRY(c, cudaStreamWaitEvent(c->ce_up, ev, 0));  // unpack writes .grad
+    for (size_t k = 1; k < c->rr_stream.size(); ++k) CUDA_TRY(c, cudaStreamWaitEvent(c->rr_stream[k], ev, 0));
+    for (int k = 1; k < kMaxLanes; ++k)
+      if (c->lane_stream[k]) CUDA_TRY(c, cudaStreamWaitEvent(c->lane_stream[k], ev, 0));
+    for (cudaStream_t q : c->ce2_rs) CUDA_TRY(c, cudaStreamWaitEvent(q, ev, 0));
+  }
+  c->unwaited.clear();
+  if (c->world == 1 && !c->emulated) {
+    // group maximal runs of world-1 fused buckets (slot table <= kMaxSlotsPerLaunch)
+    int b = b0;
+    while (b < b1) {
+      if (c->buckets[b].algo != DDP_ALGO_ONESHOT) {
+        if (ddp_status_t st = launch_device(c, b)) return st;
+        ++b;
+        continue;
+      }
+      int e = b;
+      size_t slots = 0;
+      while (e < b1 && c->buckets[e].algo == DDP_ALGO_ONESHOT &&
+             slots + c->buckets[e].params.size() <= (size_t)kMaxSlotsPerLaunch)
+        slots += c->buckets[e++].params.size();
+      if (ddp_status_t st = launch_local_group(c, b, e)) return st;
+      b = e;
+    }
+    return DDP_OK;
+  }
+  for (int b = b0; b < b1; ++b)
+    if (ddp_status_t st = launch_device(c, b)) return st;
+  return DDP_OK;
+}
+
+// find_unused, end of a synced pass: local bitmap -> device (non-blocking
+// copy from pinned host memory), ONE extra allreduce (sum) of the bitmap on the
+// comm stream after every bucket, write-back of the locally-unused parameters
+// that some rank used, and the summed bitmap back to the host for
+// ddp_global_unused.  Then the local bitmap restarts (next synced window).
+ddp_status_t finish_unused(ddp_ctx* c) {
+  const int32_t n = (int32_t)c->numel.size();
+  if (c->bitmap_valid) CUDA_TRY(c, cudaEventSynchronize(c->bitmap_done));  // host buffers reusable
+  for (int32_t p = 0; p < n; ++p) c->bitmap_host[p] = c->used_local[p];
+  int32_t* dev_bitmap = reinterpret_cast<int32_t*>(static_cast<char*>(c->storage[c->rank]) + c->bitmap_off);
+  CUDA_TRY(c, cudaMemcpyAsync(dev_bitmap, c->bitmap_host, (size_t)n * 4, cudaMemcpyHostToDevice, c->comm));
+  NCCL_TRY(c, ncclAllReduce(dev_bitmap, dev_bitmap, (size_t)n, ncclInt32, ncclSum, c->nccl, c->comm));
+  std::vector<const void*> src;
+  std::vector<void*> dst;
+  std::vector<int32_t> prm;
+  std::vector<int64_t> cnt;
+  for (size_t k = 0; k < c->un_param.size(); ++k) {
+    if (!c->un_dst[k]) continue;  // no gradient buffer: nothing to write back
+    src.push_back(c->un_src[k]);
+    dst.push_back(c->un_dst[k]);
+    prm.push_back(c->un_param[k]);
+    cnt.push_back(c->un_numel[k]);
+  }
+  const UnusedView uv{src.data(), dst.data(), prm.data(), cnt.data(), (int32_t)src.size()};
+  CUDA_TRY(c, launch_unused_fixup(c->dtype, uv, dev_bitmap, (int)c->pack_ctas, c->comm));
+  CUDA_TRY(c, cudaMemcpyAsync(c->global_host, dev_bitmap, (size_t)n * 4, cudaMemcpyDeviceToHost, c->comm));
+  CUDA_TRY(c, cudaEventRecord(c->bitmap_done, c->comm));
+  c->bitmap_valid = true;
+  std::fill(c->used_local.begin(), c->used_local.end(), 0);
+  return DDP_OK;
+}
+
+}  // namespace b200ddp
