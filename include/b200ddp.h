@@ -99,11 +99,14 @@ enum {
                                    as bf16 through the CE exchange (every bucket uses DDP_ALGO_CE at
                                    world > 1): s_q = RNE_bf16(g_q * fl(1/W)), fp32 rank-order sum,
                                    fp32 result (oracle O-8).  fp32 contexts only; layout key */
-  DDP_OPT_LANES = 16            /* P2P / NVLS kernels of bucket b run on stream (lane) b mod LANES,
+  DDP_OPT_LANES = 16,           /* P2P / NVLS kernels of bucket b run on stream (lane) b mod LANES,
                                    each lane with its own barrier flags, sequence and staging, so
                                    consecutive buckets' kernels overlap.  1..4, default 4; layout key.
                                    Lanes are used only while LANES x COMM_CTAS <= 148 (all lanes'
                                    spinning kernels must fit on the SMs at once) */
+  DDP_OPT_LOW_PRIORITY = 17     /* 1: the library's own streams (lanes, copy-engine, round-robin) are
+                                   created at the lowest priority instead of the highest, so queued
+                                   backward kernels are scheduled first; before binding only */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.

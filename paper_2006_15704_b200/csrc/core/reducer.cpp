@@ -495,6 +495,7 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
   if (c->nccl_comms > 1) {  // round-robin groups: split k-1 more communicators off the first
     int lo = 0, hi = 0;
     CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    if (c->low_priority) hi = lo;  // side streams at the lowest priority
     c->rr_comm.assign((size_t)c->nccl_comms, nullptr);
     c->rr_stream.assign((size_t)c->nccl_comms, nullptr);
     c->rr_done.assign((size_t)c->nccl_comms, nullptr);
@@ -512,6 +513,7 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
   if (c->world > 1 && c->lanes > 1) {
     int lo = 0, hi = 0;
     CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    if (c->low_priority) hi = lo;  // side streams at the lowest priority
     for (int k = 1; k < c->lanes; ++k) {
       CUDA_TRY(c, cudaStreamCreateWithPriority(&c->lane_stream[k], cudaStreamNonBlocking, hi));
       CUDA_TRY(c, cudaEventCreateWithFlags(&c->lane_done[k], cudaEventDisableTiming));
@@ -524,6 +526,7 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
   if (any_ce) {
     int lo = 0, hi = 0;
     CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    if (c->low_priority) hi = lo;  // side streams at the lowest priority
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_red, cudaStreamNonBlocking, hi));
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_pack, cudaStreamNonBlocking, hi));
     c->ce_packed.assign(c->buckets.size(), nullptr);
@@ -748,6 +751,10 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       if (v < 0) return fail(DDP_ERR_INVALID_ARG, "negative CE_DIRECT_BYTES");
       c->ce_direct = v;
       break;
+    case DDP_OPT_LOW_PRIORITY:
+      if (c->bound) return fail(DDP_ERR_STATE, "LOW_PRIORITY is fixed once bound");
+      c->low_priority = v ? 1 : 0;
+      return DDP_OK;
     case DDP_OPT_LANES:
       if (v < 1 || v > kMaxLanes) return fail(DDP_ERR_INVALID_ARG, "LANES must be in [1, 4]");
       c->lanes = v;
@@ -807,6 +814,7 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_CE_DIRECT_BYTES: *v = c->ce_direct; break;
     case DDP_OPT_WIRE_BF16: *v = c->wire_bf16; break;
     case DDP_OPT_LANES: *v = c->lanes; break;
+    case DDP_OPT_LOW_PRIORITY: *v = c->low_priority; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;
