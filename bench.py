@@ -295,6 +295,16 @@ def run_ours(a):
         times = timed(step, a.steps)
         barrier()
     ms = max_over_ranks(sum(times) / len(times))
+    # host cost of issuing one step (ready signals + finalize), no device sync inside:
+    # if it approaches the device time the step is host-bound
+    torch.cuda.synchronize(dev)
+    hs = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        step()
+        hs.append((time.perf_counter() - t0) * 1e3)
+        torch.cuda.synchronize(dev)
+    host_ms = max_over_ranks(sorted(hs)[len(hs) // 2])
 
     # ---- per-kernel device time (profile events on the comm stream) -----------------
     L.ddp_set_option(red.ctx, L.OPT_PROFILE, 1)
@@ -478,6 +488,7 @@ def run_ours(a):
             "e2e": e2e,
             "gpu_launches": int(round(launches_per_step * a.steps)),
             "host_us_per_grad_ready": host_us,
+            "host_ms_to_issue_step": host_ms,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
