@@ -181,10 +181,11 @@ ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
   prof_end(c, c->ce_pack);
   CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
   // reduce-scatter on the CE2 copy stream(s); each transfer is followed by its peer's flag
+  const size_t nst = c->ce2_rs.size();
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
-    cudaStream_t q = c->ce2_rs[(i - 1) % c->ce2_rs.size()];
-    CUDA_TRY(c, cudaStreamWaitEvent(q, c->ce_packed[b], 0));
+    cudaStream_t q = c->ce2_rs[(i - 1) % nst];
+    if ((size_t)(i - 1) < nst) CUDA_TRY(c, cudaStreamWaitEvent(q, c->ce_packed[b], 0));  // once per stream
     prof_begin(c, 4, q);
     if (shard_len(j) > 0)
       CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->storage[j]) + bk.ce_off + half + r * bk.ce_stride,
@@ -207,8 +208,8 @@ ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
   // all-gather the reduced own shard into every peer's bucket
   for (int i = 1; i < W; ++i) {
     const int j = (r + i) % W;
-    cudaStream_t q = c->ce2_ag[(i - 1) % c->ce2_ag.size()];
-    CUDA_TRY(c, cudaStreamWaitEvent(q, c->ce_reduced[b], 0));
+    cudaStream_t q = c->ce2_ag[(i - 1) % nst];
+    if ((size_t)(i - 1) < nst) CUDA_TRY(c, cudaStreamWaitEvent(q, c->ce_reduced[b], 0));
     prof_begin(c, 4, q);
     if (shard_len(r) > 0)
       CUDA_TRY(c, cudaMemcpyAsync(static_cast<char*>(c->storage[j]) + bk.byte_off + r * L * e, own + r * L * e,
