@@ -54,7 +54,8 @@ def parse():
     ap.add_argument("--pack-ctas", type=int, default=0)
     ap.add_argument("--stage-kib", type=int, default=0)
     ap.add_argument("--ce-streams", type=int, default=0)
-    ap.add_argument("--low-priority", action="store_true", help="communication streams at the lowest priority")
+    ap.add_argument("--high-priority", action="store_true",
+                    help="communication streams at the highest priority (default: lowest)")
     ap.add_argument("--lanes", type=int, default=0, help="P2P/NVLS kernel lanes (streams)")
     ap.add_argument("--wire-bf16", action="store_true", help="N-3: fp32 gradients travel as bf16 (CE exchange)")
     ap.add_argument("--ce-direct-mib", type=float, default=-1, help="CE: copy gradients >= this straight from .grad")
@@ -223,8 +224,8 @@ def run_ours(a):
         opts[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
     if a.ce_streams:
         opts[L.OPT_CE_STREAMS] = a.ce_streams
-    if a.low_priority:
-        opts[L.OPT_LOW_PRIORITY] = 1
+    if a.high_priority:
+        opts[L.OPT_LOW_PRIORITY] = 0
     if a.lanes:
         opts[L.OPT_LANES] = a.lanes
     if a.wire_bf16:
@@ -713,8 +714,8 @@ def _opts(a):
         o[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
     if a.ce_streams:
         o[L.OPT_CE_STREAMS] = a.ce_streams
-    if a.low_priority:
-        o[L.OPT_LOW_PRIORITY] = 1
+    if a.high_priority:
+        o[L.OPT_LOW_PRIORITY] = 0
     if a.lanes:
         o[L.OPT_LANES] = a.lanes
     if a.wire_bf16:

@@ -104,9 +104,9 @@ enum {
                                    consecutive buckets' kernels overlap.  1..4, default 4; layout key.
                                    Lanes are used only while LANES x COMM_CTAS <= 148 (all lanes'
                                    spinning kernels must fit on the SMs at once) */
-  DDP_OPT_LOW_PRIORITY = 17     /* 1: the library's own streams (lanes, copy-engine, round-robin) are
-                                   created at the lowest priority instead of the highest, so queued
-                                   backward kernels are scheduled first; before binding only */
+  DDP_OPT_LOW_PRIORITY = 17     /* 1 (default): the library's own streams (lanes, copy-engine,
+                                   round-robin) are created at the lowest priority, so queued backward
+                                   kernels are scheduled first; 0: highest.  Before binding only */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.

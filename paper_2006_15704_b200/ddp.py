@@ -65,7 +65,7 @@ class GradReducer:
             for k, v in (options or {}).items():
                 L.ddp_set_option(self.ctx, k, v)
             self.storage_bytes = L.ddp_storage_bytes(self.ctx)
-            low = bool((options or {}).get(L.OPT_LOW_PRIORITY))
+            low = bool((options or {}).get(L.OPT_LOW_PRIORITY, 1))   # the library's default
             self.comm_stream = comm_stream or torch.cuda.Stream(device=self.device, priority=0 if low else -1)
             nccl_id = L.ddp_get_nccl_id() if self.rank == 0 else None
             mc = 0
