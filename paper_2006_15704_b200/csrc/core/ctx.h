@@ -149,6 +149,7 @@ struct ddp_ctx {
   uint64_t p2p_launches[kMaxLanes] = {};
   cudaStream_t lane_stream[kMaxLanes] = {};  // [0] = comm
   cudaEvent_t lane_done[kMaxLanes] = {};
+  cudaEvent_t lane_tail[kMaxLanes] = {};  // drains the lanes before the last bucket's kernel
   bool lane_used[kMaxLanes] = {};
   uint32_t* err_host = nullptr;
   uint32_t* err_dev = nullptr;

@@ -262,6 +262,16 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   const int ln = (c->emulated || c->world == 1) ? 0 : b % nl;
   cudaStream_t ls = ln == 0 ? c->comm : c->lane_stream[ln];
   if (ln) c->lane_used[ln] = true;
+  if (b == (int)c->buckets.size() - 1 && nl > 1 && !c->emulated) {
+    // the last bucket's kernel uses every SM (max_ctas_for): let the other lanes'
+    // spinning kernels finish first, so all of its CTAs can be resident together
+    for (int k = 0; k < nl; ++k) {
+      if (k == ln) continue;
+      cudaStream_t ks = k == 0 ? c->comm : c->lane_stream[k];
+      CUDA_TRY(c, cudaEventRecord(c->lane_tail[k], ks));
+      CUDA_TRY(c, cudaStreamWaitEvent(ls, c->lane_tail[k], 0));
+    }
+  }
   P2PLaunch a{};
   for (int r = 0; r < c->world; ++r) a.storage[r] = c->storage[r];
   a.flags_byte_off = c->flags_off + ln * kFlagsBytes;

@@ -127,8 +127,12 @@ void grid_for(const ddp_ctx* c, Bucket& bk, int max_ctas) {
   bk.stages = (int32_t)cdiv(Q, bk.sub);
 }
 
+// The last bucket holds the first-registered parameters: its sync starts when
+// backward has ended and overlaps nothing, so its kernel takes every SM (it is
+// launched after the other lanes have drained, exchange.cpp).
 int max_ctas_for(const ddp_ctx* c, const Bucket& bk) {
-  int m = c->world == 1 ? (int)c->pack_ctas : (int)std::min<int64_t>(c->comm_ctas, kMaxCtas);
+  const bool last = &bk == &c->buckets.back() && c->world > 1;
+  int m = c->world == 1 ? (int)c->pack_ctas : last ? std::min(148, kMaxCtas) : (int)std::min<int64_t>(c->comm_ctas, kMaxCtas);
   if (c->emulated) {
     const int e = emulated_max_ctas(bk.algo, c->dtype, (int)bk.params.size(), c->world);
     m = std::min(m, std::max(1, e));
@@ -400,6 +404,9 @@ void ddp_destroy(ddp_ctx_t* c) {
     }
     if (c->lane_done[k]) cudaEventDestroy(c->lane_done[k]);
   }
+  for (int k = 0; k < kMaxLanes; ++k) {
+    if (c->lane_tail[k]) cudaEventDestroy(c->lane_tail[k]);
+  }
   for (cudaEvent_t e : c->ce_packed) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ce_copied) cudaEventDestroy(e);
   if (c->ce_red_done) cudaEventDestroy(c->ce_red_done);
@@ -518,6 +525,7 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
       CUDA_TRY(c, cudaStreamCreateWithPriority(&c->lane_stream[k], cudaStreamNonBlocking, hi));
       CUDA_TRY(c, cudaEventCreateWithFlags(&c->lane_done[k], cudaEventDisableTiming));
     }
+    for (int k = 0; k < c->lanes; ++k) CUDA_TRY(c, cudaEventCreateWithFlags(&c->lane_tail[k], cudaEventDisableTiming));
   }
   CUDA_TRY(c, cudaMemsetAsync(mine + c->ce_flags_off, 0, (size_t)c->buckets.size() * kMaxWorld * 3 * 4, c->comm));
   bool any_ce = false;
