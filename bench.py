@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--pack-ctas", type=int, default=0)
     ap.add_argument("--stage-kib", type=int, default=0)
     ap.add_argument("--ce-streams", type=int, default=0)
+    ap.add_argument("--throughput-policy", action="store_true",
+                    help="exposed-time runs: DDP without the overlap policy (PREFER_OVERLAP=0)")
     ap.add_argument("--high-priority", action="store_true",
                     help="communication streams at the highest priority (default: lowest)")
     ap.add_argument("--lanes", type=int, default=0, help="P2P/NVLS kernel lanes (streams)")
@@ -224,6 +226,8 @@ def run_ours(a):
         opts[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
     if a.ce_streams:
         opts[L.OPT_CE_STREAMS] = a.ce_streams
+    if a.throughput_policy:
+        opts[L.OPT_PREFER_OVERLAP] = 0
     if a.high_priority:
         opts[L.OPT_LOW_PRIORITY] = 0
     if a.lanes:
@@ -714,6 +718,8 @@ def _opts(a):
         o[L.OPT_P2P_STAGE_BYTES] = a.stage_kib * 1024
     if a.ce_streams:
         o[L.OPT_CE_STREAMS] = a.ce_streams
+    if a.throughput_policy:
+        o[L.OPT_PREFER_OVERLAP] = 0
     if a.high_priority:
         o[L.OPT_LOW_PRIORITY] = 0
     if a.lanes:

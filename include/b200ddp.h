@@ -104,9 +104,15 @@ enum {
                                    consecutive buckets' kernels overlap.  1..4, default 4; layout key.
                                    Lanes are used only while LANES x COMM_CTAS <= 148 (all lanes'
                                    spinning kernels must fit on the SMs at once) */
-  DDP_OPT_LOW_PRIORITY = 17     /* 1 (default): the library's own streams (lanes, copy-engine,
+  DDP_OPT_LOW_PRIORITY = 17,    /* 1 (default): the library's own streams (lanes, copy-engine,
                                    round-robin) are created at the lowest priority, so queued backward
                                    kernels are scheduled first; 0: highest.  Before binding only */
+  DDP_OPT_PREFER_OVERLAP = 18   /* automatic policy for gradients produced by a running backward
+                                   (the front end's DistributedDataParallel sets it): at world > 2
+                                   every bucket but the last uses the SM-free copy-engine two-shot
+                                   (CE2), the last one the fastest kernel on every SM.  Default 0:
+                                   the policy that is fastest when all buckets are ready at once.
+                                   Layout key */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.

@@ -98,6 +98,11 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
     // measured at W=4, profiles/r01_n4.md); from W=6 NVLS's (1+1/W) S is >= 1.5x
     // fewer NVLink bytes, which outweighs its lower per-byte rate seen at W=4
     a = c->world == 2 ? DDP_ALGO_CE : (c->multicast && c->world >= 6) ? DDP_ALGO_NVLS : DDP_ALGO_TWOSHOT;
+    // PREFER_OVERLAP (buckets synced while backward still runs): the copy-engine
+    // two-shot keeps the SMs with autograd (lowest exposed time at W=4,
+    // profiles/r01_n4.md); the last bucket overlaps nothing and keeps the
+    // fastest kernel on every SM
+    if (c->prefer_overlap && c->world > 2 && &bk != &c->buckets.back()) a = DDP_ALGO_CE2;
   } else {
     a = DDP_ALGO_NCCL;
   }
@@ -298,7 +303,7 @@ ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s, b
 bool is_layout_key(int32_t k) {
   return k == DDP_OPT_P2P_ONESHOT_MAX || k == DDP_OPT_P2P_TWOSHOT_MAX || k == DDP_OPT_ALGO ||
          k == DDP_OPT_FIND_UNUSED || k == DDP_OPT_MULTICAST || k == DDP_OPT_CE_DIRECT_BYTES ||
-         k == DDP_OPT_WIRE_BF16 || k == DDP_OPT_LANES;
+         k == DDP_OPT_WIRE_BF16 || k == DDP_OPT_LANES || k == DDP_OPT_PREFER_OVERLAP;
 }
 
 }  // namespace
@@ -759,6 +764,9 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       if (v < 0) return fail(DDP_ERR_INVALID_ARG, "negative CE_DIRECT_BYTES");
       c->ce_direct = v;
       break;
+    case DDP_OPT_PREFER_OVERLAP:
+      c->prefer_overlap = v ? 1 : 0;
+      break;
     case DDP_OPT_LOW_PRIORITY:
       if (c->bound) return fail(DDP_ERR_STATE, "LOW_PRIORITY is fixed once bound");
       c->low_priority = v ? 1 : 0;
@@ -823,6 +831,7 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_WIRE_BF16: *v = c->wire_bf16; break;
     case DDP_OPT_LANES: *v = c->lanes; break;
     case DDP_OPT_LOW_PRIORITY: *v = c->low_priority; break;
+    case DDP_OPT_PREFER_OVERLAP: *v = c->prefer_overlap; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;

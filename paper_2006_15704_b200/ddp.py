@@ -221,6 +221,9 @@ class DistributedDataParallel(torch.nn.Module):
         options = dict(options or {})
         if find_unused_parameters:
             options[L.OPT_FIND_UNUSED] = 1
+        # DDP's buckets are synced while backward still runs: the overlap policy
+        # (SM-free exchanges except for the last bucket) unless the caller chose
+        options.setdefault(L.OPT_PREFER_OVERLAP, 1)
         self.module = module
         self.params = [p for p in module.parameters() if p.requires_grad]
         dtypes = {p.dtype for p in self.params}
