@@ -117,7 +117,8 @@ def test_multigpu_parity(world):
             ("resnet50", "fp32", 5 * MIB, L.ALGO_ONESHOT, 2, {L.OPT_LANES: 1}),
             ("toy", "bf16", 4096, L.ALGO_CE2, 3), ("resnet50", "fp32", 25 * MIB, L.ALGO_CE2, 3),
             ("bert_large", "bf16", 25 * MIB, L.ALGO_CE2, 1),
-            ("resnet50", "fp32", 5 * MIB, L.ALGO_AUTO, 2, {L.OPT_PREFER_OVERLAP: 1})]
+            ("resnet50", "fp32", 5 * MIB, L.ALGO_AUTO, 2, {L.OPT_PREFER_OVERLAP: 1}),
+            ("bert_large", "fp32", 25 * MIB, L.ALGO_AUTO, 1)]      # the bench's BERT config as launched
     outs = _run(world, cfgs)
     for ci, cfg in enumerate(cfgs):
         model, dtype, cap, algo, iters = cfg[:5]
