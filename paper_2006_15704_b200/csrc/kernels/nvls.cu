@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       hi = (hi + VE - 1) / VE * VE;
       char* mcb = static_cast<char*>(a.mc) + a.bucket_byte_off;
       const int64_t v0 = lo / VE, nv = hi / VE - v0;
-      constexpr int U = 4;
+      constexpr int U = 8;  // ld_reduce is a round trip through the switch: keep many in flight
       int64_t v = threadIdx.x;
       for (; v + (U - 1) * (int64_t)blockDim.x < nv; v += U * (int64_t)blockDim.x) {
         uint4 x[U];
