@@ -99,7 +99,7 @@ __device__ __forceinline__ void cta_xfer(T* const (&dst)[ND], const T* const (&s
   constexpr int VE = E::VE;
   // 4 vectors per thread in flight for a plain copy: with many small CTAs this
   // measured best on B200 (tools/local_probe.cu; profiles/r01_local_u.md)
-  constexpr int U = UF ? UF : NS == 1 ? 4 : (NS >= 4 ? 1 : 4 / NS);
+  constexpr int U = UF ? UF : NS <= 2 ? 4 : (NS >= 4 ? 1 : 4 / NS);
   const int tid = threadIdx.x, nt = blockDim.x;
   if (n <= 0) return;
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(dst[0]) & 15;

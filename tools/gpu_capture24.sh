@@ -1,0 +1,9 @@
+# 4 GPUs: NVLS with 8 multimem vectors in flight (parity + synthetic step).
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_multigpu.py -x -q -p no:cacheprovider -k "4" > gpurun_out/n4c24_pytest.log 2>&1; echo pytest=$? >> gpurun_out/n4c24_pytest.log
+T4="timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29511"
+R=gpurun_out/n4c24_bench.jsonl; rm -f $R
+for args in "--algo 5 --workload bert_large" "--algo 5"; do
+  echo "ARGS: N4 $args" >> $R
+  $T4 bench.py --gpus 4 --warmup 5 --no-e2e --exposed-model none $args >> $R 2>>gpurun_out/n4c24_bench.err
+done
