@@ -262,7 +262,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   const int ln = (c->emulated || c->world == 1) ? 0 : b % nl;
   cudaStream_t ls = ln == 0 ? c->comm : c->lane_stream[ln];
   if (ln) c->lane_used[ln] = true;
-  if (b == (int)c->buckets.size() - 1 && nl > 1 && !c->emulated) {
+  if (b == (int)c->buckets.size() - 1 && nl > 1 && c->world > 1 && !c->emulated) {
     // the last bucket's kernel uses every SM (max_ctas_for): let the other lanes'
     // spinning kernels finish first, so all of its CTAs can be resident together
     for (int k = 0; k < nl; ++k) {
