@@ -795,7 +795,7 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       regrid(c);
       return DDP_OK;
     case DDP_OPT_PACK_CTAS:
-      if (v < 1 || v > 148 * 32) return fail(DDP_ERR_INVALID_ARG, "PACK_CTAS must be in [1, 4736]");
+      if (v < 1 || v > 148 * 64) return fail(DDP_ERR_INVALID_ARG, "PACK_CTAS must be in [1, 9472]");
       c->pack_ctas = v;
       regrid(c);
       return DDP_OK;
