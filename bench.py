@@ -357,7 +357,7 @@ def run_ours(a):
             for s_ in range(L.ddp_bucket_info(red.ctx, b)[1]):
                 p, _ = L.ddp_bucket_slot(red.ctx, b, s_)
                 small += ns[p] * esize if ns[p] * esize < L.ddp_get_option(red.ctx, L.OPT_CE_DIRECT_BYTES) else 0
-    by = {x: sum(n * esize for n, y in zip(bnumel, algos) if y == x) for x in ("nccl", "oneshot", "twoshot", "ce", "nvls", "push", "ce2")}
+    by = {x: sum(n * esize for n, y in zip(bnumel, algos) if y == x) for x in ("nccl", "oneshot", "twoshot", "ce", "nvls", "push", "ce2", "nvls2")}
 
     def kind_bytes(kind):
         """(algorithmic bytes per step, bound, rule) of one profile kind."""
@@ -366,13 +366,13 @@ def run_ours(a):
         if kind == "pack":
             if a.wire_bf16:
                 return 1.5 * by["ce"], "hbm", "fp32 read + bf16 write of every gradient (compressed wire)"
-            return (2 * (by["nccl"] + small + by["ce2"]), "hbm",
-                    "2 x bytes packed (NCCL and CE2 buckets; CE small gradients)")
+            return (2 * (by["nccl"] + small + by["ce2"] + by["nvls2"]), "hbm",
+                    "2 x bytes packed (NCCL, CE2 and NVLS2 buckets; CE small gradients)")
         if kind == "unpack":
-            return 2 * (by["nccl"] + by["ce2"]), "hbm", "2 x bucket bytes"
+            return 2 * (by["nccl"] + by["ce2"] + by["nvls2"]), "hbm", "2 x bucket bytes"
         if kind == "p2p_fused":
             return (by["oneshot"] * (world - 1) + by["twoshot"] * 2 * (world - 1) / world
-                    + by["nvls"] * (1 + 1 / world), "nvlink",
+                    + (by["nvls"] + by["nvls2"]) * (1 + 1 / world), "nvlink",
                     "NVLink bytes per direction: one-shot (W-1)S, two-shot 2(W-1)/W S, NVLS (1+1/W)S")
         if kind == "ce_copy":
             wf = 0.5 if a.wire_bf16 else 1.0   # the compressed wire carries bf16

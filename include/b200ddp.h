@@ -75,7 +75,8 @@ enum {
   DDP_OPT_PROFILE = 6,          /* 1: time every device launch with CUDA events */
   DDP_OPT_ALGO = 7,             /* force the bucket allreduce: 0 auto, 1 NCCL, 2 one-shot, 3 two-shot,
                                    4 copy-engine one-shot (world > 1), 5 NVLS (needs MULTICAST),
-                                   6 SM push + stream-ordered reduce, 7 copy-engine two-shot (world > 1) */
+                                   6 SM push + stream-ordered reduce, 7 copy-engine two-shot,
+                                   8 stream-ordered NVLS (world > 1) */
   DDP_OPT_PACK_CTAS = 8,        /* max CTAs of pack/unpack kernels and of P2P kernels at world 1 */
   DDP_OPT_P2P_STAGE_BYTES = 9,  /* 0 (default): one pipeline stage per CTA chunk; else split each
                                    CTA chunk into stages of this many bytes (one sync per stage) */
@@ -131,9 +132,12 @@ enum {
  *            b's reduction on the second stream.
  *   CE2:     copy-engine two-shot: pack kernel -> reduce-scatter copies of shards -> rank-order
  *            shard reduce kernel -> all-gather copies -> unpack kernel, five streams ordered by
- *            stream memory operations; 2(W-1)/W S NVLink bytes per direction, no SM waits. */
+ *            stream memory operations; 2(W-1)/W S NVLink bytes per direction, no SM waits.
+ *   NVLS2:   stream-ordered NVLS: pack kernel -> [stream memops] multimem.ld_reduce/st kernel on the
+ *            own shard -> [stream memops] unpack kernel, three streams, no SM waits; (1+1/W) S
+ *            NVLink bytes per direction.  Needs DDP_OPT_MULTICAST; otherwise resolves to CE2. */
 enum { DDP_ALGO_AUTO = 0, DDP_ALGO_NCCL = 1, DDP_ALGO_ONESHOT = 2, DDP_ALGO_TWOSHOT = 3, DDP_ALGO_CE = 4,
-       DDP_ALGO_NVLS = 5, DDP_ALGO_PUSH = 6, DDP_ALGO_CE2 = 7 };
+       DDP_ALGO_NVLS = 5, DDP_ALGO_PUSH = 6, DDP_ALGO_CE2 = 7, DDP_ALGO_NVLS2 = 8 };
 
 /* ---- construction (host only, deterministic, touches no GPU) -------------
  * Bucket assignment (Alg. 1 "allocate parameters to buckets in the

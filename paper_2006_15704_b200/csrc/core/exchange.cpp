@@ -228,6 +228,48 @@ ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
   return DDP_OK;
 }
 
+// Stream-ordered NVLS (NVLS2): the three phases of the NVLS kernel as separate
+// kernels on three streams, ordered across ranks by stream memory operations,
+// so no kernel waits inside and consecutive buckets pipeline:
+//   pack stream:    pack x 1/W into the own bucket; "packed" flag to every peer
+//   reduce stream:  [wait all packed] own shard: multimem.ld_reduce + multimem.st
+//                   through the multicast address; "stored" flag to every peer
+//   unpack stream:  [wait all stored] own bucket -> .grad
+// Reuse: the next pass packs the bucket after this rank's unpack (finalize),
+// which followed every peer's "stored", which followed its ld_reduce reads.
+ddp_status_t launch_nvls2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
+  Bucket& bk = c->buckets[b];
+  const int W = c->world, r = c->rank;
+  const uint32_t v = ++bk.ce_count;
+  char* own = static_cast<char*>(c->storage[r]) + bk.byte_off;
+  prof_begin(c, 0, c->ce_pack);
+  CUDA_TRY(c, launch_pack(c->dtype, sv, own, scale, (int)c->pack_ctas, c->ce_pack));
+  prof_end(c, c->ce_pack);
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_write(c, c->ce_pack, ce_flag(c, (r + i) % W, 0, b, r), v)) return st;
+  CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_red, c->ce_packed[b], 0));
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_wait(c, c->ce_red, ce_flag(c, r, 0, b, (r + i) % W), v)) return st;
+  const int64_t L = bk.shard;
+  const int64_t lo = std::min<int64_t>(r * L, bk.numel), hi = std::min<int64_t>(lo + L, bk.numel);
+  prof_begin(c, 3, c->ce_red);
+  CUDA_TRY(c, launch_nvls_reduce(c->dtype, static_cast<char*>(c->mc) + bk.byte_off, lo, hi, (int)c->pack_ctas,
+                                 c->ce_red));
+  prof_end(c, c->ce_red);
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_write(c, c->ce_red, ce_flag(c, (r + i) % W, 2, b, r), v)) return st;
+  CUDA_TRY(c, cudaEventRecord(c->ce_reduced[b], c->ce_red));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_up, c->ce_reduced[b], 0));
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_wait(c, c->ce_up, ce_flag(c, r, 2, b, (r + i) % W), v)) return st;
+  prof_begin(c, 2, c->ce_up);
+  CUDA_TRY(c, launch_unpack(c->dtype, sv, own, (int)c->pack_ctas, c->ce_up));
+  prof_end(c, c->ce_up);
+  c->ce2_used = true;  // joins ce_up at finalize
+  return DDP_OK;
+}
+
 // ---- a3/a4/a6 device work for one bucket -------------------------------------
 ddp_status_t launch_device(ddp_ctx* c, int b) {
   Bucket& bk = c->buckets[b];
@@ -236,6 +278,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   char* mine = static_cast<char*>(c->storage[c->rank]);
   if (bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH) return launch_ce(c, b);
   if (bk.algo == DDP_ALGO_CE2) return launch_ce2(c, b, sv, scale);
+  if (bk.algo == DDP_ALGO_NVLS2) return launch_nvls2(c, b, sv, scale);
   if (bk.algo == DDP_ALGO_NCCL) {
     void* buf = mine + bk.byte_off;
     const size_t k = c->rr_comm.empty() ? 0 : (size_t)b % c->rr_comm.size();

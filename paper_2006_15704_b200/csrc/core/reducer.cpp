@@ -81,8 +81,10 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   int a;
   if (c->algo != DDP_ALGO_AUTO) {
     a = (int)c->algo;
-    if (c->world == 1 && (a == DDP_ALGO_CE || a == DDP_ALGO_NVLS || a == DDP_ALGO_PUSH || a == DDP_ALGO_CE2))
+    if (c->world == 1 && (a == DDP_ALGO_CE || a == DDP_ALGO_NVLS || a == DDP_ALGO_PUSH || a == DDP_ALGO_CE2 ||
+                          a == DDP_ALGO_NVLS2))
       a = DDP_ALGO_ONESHOT;
+    if (a == DDP_ALGO_NVLS2 && !c->multicast) a = DDP_ALGO_CE2;
     if (c->world > 1 && c->wire_bf16) a = DDP_ALGO_CE;  // the compressed wire is a CE feature
     if (a == DDP_ALGO_NVLS && !c->multicast) a = DDP_ALGO_TWOSHOT;
   } else if (c->world == 1) {
@@ -114,7 +116,7 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
 
 // Grid of a P2P launch: per-CTA chunks of >= kMinChunkElems, 256-element aligned.
 void grid_for(const ddp_ctx* c, Bucket& bk, int max_ctas) {
-  if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE2) {
+  if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE2 || bk.algo == DDP_ALGO_NVLS2) {
     bk.ctas = 0;
     bk.chunk = 0;
     if (bk.algo == DDP_ALGO_NCCL) bk.shard = 0;
@@ -170,6 +172,10 @@ void plan(ddp_ctx* c) {
     bk.ce_stride = 0;
     bk.ce_wire.clear();
     bk.ce_direct.clear();
+    if (bk.algo == DDP_ALGO_NVLS2) {  // no staging: the switch reads every rank's bucket
+      bk.shard = align_up(cdiv(bk.numel, c->world), kAlignElems);
+      continue;
+    }
     if (bk.algo == DDP_ALGO_CE2) {  // double-buffered reduce-scatter staging: [2][W] shard slots
       const int64_t L = align_up(cdiv(bk.numel, c->world), kAlignElems);
       bk.shard = L;
@@ -535,7 +541,8 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
   CUDA_TRY(c, cudaMemsetAsync(mine + c->ce_flags_off, 0, (size_t)c->buckets.size() * kMaxWorld * 3 * 4, c->comm));
   bool any_ce = false;
   for (const Bucket& bk : c->buckets)
-    any_ce |= bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH || bk.algo == DDP_ALGO_CE2;
+    any_ce |= bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH || bk.algo == DDP_ALGO_CE2 ||
+              bk.algo == DDP_ALGO_NVLS2;
   if (any_ce) {
     int lo = 0, hi = 0;
     CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -588,7 +595,8 @@ ddp_status_t ddp_bind_emulated(ddp_ctx_t* c, int32_t device, void* comm_stream, 
       return fail(DDP_ERR_INVALID_ARG, "storages must be non-null and 256-B aligned");
   }
   for (const Bucket& bk : c->buckets)
-    if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH || bk.algo == DDP_ALGO_CE2)
+    if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH || bk.algo == DDP_ALGO_CE2 ||
+        bk.algo == DDP_ALGO_NVLS2)
       return fail(DDP_ERR_UNSUPPORTED, "emulation runs the one-shot / two-shot kernels only (set DDP_OPT_ALGO)");
   if (c->find_unused) return fail(DDP_ERR_UNSUPPORTED, "find_unused needs a real communicator (no emulation)");
   if (c->multicast) return fail(DDP_ERR_UNSUPPORTED, "NVLS needs real multicast memory (no emulation)");
@@ -751,7 +759,7 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       c->twoshot_max = v;
       break;
     case DDP_OPT_ALGO:
-      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_CE2) return fail(DDP_ERR_INVALID_ARG, "bad algo");
+      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_NVLS2) return fail(DDP_ERR_INVALID_ARG, "bad algo");
       c->algo = v;
       break;
     case DDP_OPT_FIND_UNUSED:

@@ -64,6 +64,8 @@ cudaError_t launch_unpack(int dtype, const SlotView& sv, const void* bucket, int
 cudaError_t launch_p2p(int algo, int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
 // NVLS (NVSwitch multicast) two-shot: pack -> multimem.ld_reduce + multimem.st -> unpack.
 cudaError_t launch_nvls(int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
+// NVLS2 reduce phase: bucket elements [lo, hi) through its multicast address.
+cudaError_t launch_nvls_reduce(int dtype, void* mc_bucket, int64_t lo, int64_t hi, int max_ctas, cudaStream_t s);
 // Copy-engine algorithm, SM part.  A list of gradients with their element
 // offsets inside a slot ("wire layout").
 struct CeView {

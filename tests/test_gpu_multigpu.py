@@ -118,13 +118,14 @@ def test_multigpu_parity(world):
             ("toy", "bf16", 4096, L.ALGO_CE2, 3), ("resnet50", "fp32", 25 * MIB, L.ALGO_CE2, 3),
             ("bert_large", "bf16", 25 * MIB, L.ALGO_CE2, 1),
             ("resnet50", "fp32", 5 * MIB, L.ALGO_AUTO, 2, {L.OPT_PREFER_OVERLAP: 1}),
-            ("bert_large", "fp32", 25 * MIB, L.ALGO_AUTO, 1)]      # the bench's BERT config as launched
+            ("bert_large", "fp32", 25 * MIB, L.ALGO_AUTO, 1),      # the bench's BERT config as launched
+            ("toy", "fp32", 4096, L.ALGO_NVLS2, 2), ("resnet50", "bf16", 25 * MIB, L.ALGO_NVLS2, 2)]
     outs = _run(world, cfgs)
     for ci, cfg in enumerate(cfgs):
         model, dtype, cap, algo, iters = cfg[:5]
         ns = numels(model)
         algos = outs[0][ci][1]
-        tol = any(x in ("nccl", "nvls") for x in algos)   # not rank-order sums: tolerance parity
+        tol = any(x in ("nccl", "nvls", "nvls2") for x in algos)   # not rank-order sums: tolerance parity
         wire = len(cfg) > 5 and cfg[5].get(L.OPT_WIRE_BF16)
         for it in range(iters):
             for p in range(len(ns)):
