@@ -96,10 +96,11 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   } else if (bytes <= c->twoshot_max) {
     // world 2: the copy-engine exchange moves the same (W-1) S = S bytes as any
     // algorithm, keeps the SMs free for backward and pipelines buckets
-    // (profiles/r01_n2.md).  Wider: two-shot, 2(W-1)/W S per direction (best
-    // measured at W=4, profiles/r01_n4.md); from W=6 NVLS's (1+1/W) S is >= 1.5x
-    // fewer NVLink bytes, which outweighs its lower per-byte rate seen at W=4
-    a = c->world == 2 ? DDP_ALGO_CE : (c->multicast && c->world >= 6) ? DDP_ALGO_NVLS : DDP_ALGO_TWOSHOT;
+    // (profiles/r01_n2.md).  Wider: two-shot, 2(W-1)/W S per direction — best
+    // measured at W=4 (profiles/r01_n4.md).  NVLS moves only (1+1/W) S, but the
+    // switch path ran at ~0.7x the per-byte rate of SM stores at W=4 (both the
+    // fused and the stream-ordered kernel), so it is an option, not a default
+    a = c->world == 2 ? DDP_ALGO_CE : DDP_ALGO_TWOSHOT;
     // PREFER_OVERLAP (buckets synced while backward still runs): the copy-engine
     // two-shot keeps the SMs with autograd (lowest exposed time at W=4,
     // profiles/r01_n4.md); the last bucket overlaps nothing and keeps the
