@@ -1,0 +1,9 @@
+# 2 GPUs, final verification of round 1: full GPU suite, smoke, contract lines at N=1 and N=2 (+ reference arm).
+mkdir -p gpurun_out
+timeout 1800 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/c31_pytest.log 2>&1; echo pytest=$? >> gpurun_out/c31_pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/c31_smoke.log 2>&1; echo smoke=$? >> gpurun_out/c31_smoke.log
+timeout 600 python bench.py > gpurun_out/c31_n1.json 2> gpurun_out/c31_n1.err
+timeout 600 python bench.py --impl reference > gpurun_out/c31_ref.json 2>> gpurun_out/c31_n1.err
+T="timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511"
+$T bench.py --gpus 2 > gpurun_out/c31_n2.json 2> gpurun_out/c31_n2.err
+$T bench.py --gpus 2 --workload bert_large --exposed-model bert_large > gpurun_out/c31_n2_bert.json 2>> gpurun_out/c31_n2.err
