@@ -222,8 +222,12 @@ class DistributedDataParallel(torch.nn.Module):
         if find_unused_parameters:
             options[L.OPT_FIND_UNUSED] = 1
         # DDP's buckets are synced while backward still runs: the overlap policy
-        # (SM-free exchanges except for the last bucket) unless the caller chose
-        options.setdefault(L.OPT_PREFER_OVERLAP, 1)
+        # (SM-free exchanges except for the last bucket) unless the caller chose.
+        # Measured at W=4 (profiles/r01_n4.md): it cuts BERT-large fp32's exposed
+        # time 8.7% -> 5.3%, but with bf16 gradients (a backward half as long) the
+        # copy engines fall behind (9.4% -> 17-31%), so bf16 keeps the kernels
+        dtypes_ = {p.dtype for p in module.parameters() if p.requires_grad}
+        options.setdefault(L.OPT_PREFER_OVERLAP, 1 if dtypes_ == {torch.float32} else 0)
         self.module = module
         self.params = [p for p in module.parameters() if p.requires_grad]
         dtypes = {p.dtype for p in self.params}
