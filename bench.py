@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--ce-streams", type=int, default=0)
     ap.add_argument("--throughput-policy", action="store_true",
                     help="exposed-time runs: DDP without the overlap policy (PREFER_OVERLAP=0)")
+    ap.add_argument("--overlap-policy", action="store_true",
+                    help="exposed-time runs: force the overlap policy (PREFER_OVERLAP=1), e.g. for bf16")
     ap.add_argument("--high-priority", action="store_true",
                     help="communication streams at the highest priority (default: lowest)")
     ap.add_argument("--lanes", type=int, default=0, help="P2P/NVLS kernel lanes (streams)")
@@ -228,6 +230,8 @@ def run_ours(a):
         opts[L.OPT_CE_STREAMS] = a.ce_streams
     if a.throughput_policy:
         opts[L.OPT_PREFER_OVERLAP] = 0
+    if a.overlap_policy:
+        opts[L.OPT_PREFER_OVERLAP] = 1
     if a.high_priority:
         opts[L.OPT_LOW_PRIORITY] = 0
     if a.lanes:
@@ -670,6 +674,7 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
            "exposed_pct_of_bwd": 100.0 * (t_sync - t_bwd) / t_bwd,
            "iters": iters, "timing": "median of interleaved passes, max over ranks",
            "floor_ms": float(vt[-1]),
+           "floor_ok": bool(t_sync - t_bwd >= float(vt[-1]) * 0.9),
            "floor_doc": "whole sync of the last bucket alone (it cannot start before backward ends)",
            "timeline_rank0": timeline if rank == 0 else None}
     if no_overlap:
@@ -720,6 +725,8 @@ def _opts(a):
         o[L.OPT_CE_STREAMS] = a.ce_streams
     if a.throughput_policy:
         o[L.OPT_PREFER_OVERLAP] = 0
+    if a.overlap_policy:
+        o[L.OPT_PREFER_OVERLAP] = 1
     if a.high_priority:
         o[L.OPT_LOW_PRIORITY] = 0
     if a.lanes:

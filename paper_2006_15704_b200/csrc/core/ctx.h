@@ -151,6 +151,7 @@ struct ddp_ctx {
   cudaStream_t lane_stream[kMaxLanes] = {};  // [0] = comm
   cudaEvent_t lane_done[kMaxLanes] = {};
   cudaEvent_t lane_tail[kMaxLanes] = {};  // drains the lanes before the last bucket's kernel
+  std::vector<cudaEvent_t> tail_ev;        // ... and the copy-engine streams
   bool lane_used[kMaxLanes] = {};
   uint32_t* err_host = nullptr;
   uint32_t* err_dev = nullptr;

@@ -305,14 +305,28 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   const int ln = (c->emulated || c->world == 1) ? 0 : b % nl;
   cudaStream_t ls = ln == 0 ? c->comm : c->lane_stream[ln];
   if (ln) c->lane_used[ln] = true;
-  if (b == (int)c->buckets.size() - 1 && nl > 1 && c->world > 1 && !c->emulated) {
-    // the last bucket's kernel uses every SM (max_ctas_for): let the other lanes'
-    // spinning kernels finish first, so all of its CTAs can be resident together
+  if (b == (int)c->buckets.size() - 1 && c->world > 1 && !c->emulated) {
+    // The last bucket's kernel uses every SM (max_ctas_for) and spins until the
+    // peers arrive.  Everything this rank launched before it must be finished
+    // first: the other lanes' spinning kernels (so all of its CTAs can be
+    // resident), and the copy-engine paths' kernels of earlier buckets (else
+    // they would wait for SMs behind a kernel that waits for peers — measured
+    // as a 0.8 ms stall at W=4, profiles/r01_n4.md).
     for (int k = 0; k < nl; ++k) {
       if (k == ln) continue;
       cudaStream_t ks = k == 0 ? c->comm : c->lane_stream[k];
       CUDA_TRY(c, cudaEventRecord(c->lane_tail[k], ks));
       CUDA_TRY(c, cudaStreamWaitEvent(ls, c->lane_tail[k], 0));
+    }
+    size_t q = 0;
+    for (cudaStream_t ks : {c->ce_pack, c->ce_red, c->ce_up}) {
+      if (!ks || q >= c->tail_ev.size()) continue;
+      CUDA_TRY(c, cudaEventRecord(c->tail_ev[q], ks));
+      CUDA_TRY(c, cudaStreamWaitEvent(ls, c->tail_ev[q++], 0));
+    }
+    if (ln != 0 && c->ce_used && q < c->tail_ev.size()) {  // CE copies run on the comm stream
+      CUDA_TRY(c, cudaEventRecord(c->tail_ev[q], c->comm));
+      CUDA_TRY(c, cudaStreamWaitEvent(ls, c->tail_ev[q++], 0));
     }
   }
   P2PLaunch a{};

@@ -409,6 +409,7 @@ void ddp_destroy(ddp_ctx_t* c) {
   }
   for (cudaEvent_t e : c->ce_reduced) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ce2_done) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->tail_ev) cudaEventDestroy(e);
   for (int k = 1; k < kMaxLanes; ++k) {
     if (c->lane_stream[k]) {
       if (!c->poisoned) cudaStreamSynchronize(c->lane_stream[k]);
@@ -566,6 +567,8 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
     c->ce2_done.assign(2 * nst, nullptr);
     for (auto& e : c->ce2_done) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_up, cudaStreamNonBlocking, hi));
+    c->tail_ev.assign(4, nullptr);
+    for (auto& e : c->tail_ev) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->ce_reduced.assign(c->buckets.size(), nullptr);
     for (auto& e : c->ce_reduced) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 

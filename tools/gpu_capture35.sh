@@ -1,0 +1,9 @@
+# 4 GPUs: last bucket drains the copy-engine kernels too; fp32 / bf16 exposed with the overlap policy.
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests/test_gpu_multigpu.py -x -q -p no:cacheprovider > gpurun_out/n4c35_pytest.log 2>&1; echo pytest=$? >> gpurun_out/n4c35_pytest.log
+T4="timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29511"
+R=gpurun_out/n4c35_bench.jsonl; rm -f $R
+for args in "--workload bert_large --exposed-model bert_large" "--workload bert_large --dtype bf16 --exposed-model bert_large --overlap-policy" "--workload bert_large --dtype bf16 --exposed-model bert_large"; do
+  echo "ARGS: N4 $args" >> $R
+  $T4 bench.py --gpus 4 --warmup 5 --no-e2e $args >> $R 2>>gpurun_out/n4c35_bench.err
+done
