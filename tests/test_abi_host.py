@@ -360,3 +360,24 @@ def test_rebuild_from_traced_order_launches_without_deferral():
         assert [t for _, t in tr] == [e - 1 for e in ends]
     finally:
         L.ddp_destroy(ctx)
+
+
+def test_option_and_algo_constants_match_header():
+    """The binding's OPT_* / ALGO_* constants equal the header's enum values, and
+    every option round-trips through ddp_set_option / ddp_get_option."""
+    txt = open(os.path.join(ROOT, "include", "b200ddp.h")).read()
+    opts = dict((k, int(v)) for k, v in re.findall(r"^\s*DDP_OPT_([A-Z0-9_]+)\s*=\s*(\d+)\s*,?", txt, re.M))
+    algos = dict((k, int(v)) for k, v in re.findall(r"\bDDP_ALGO_([A-Z0-9_]+)\s*=\s*(\d+)\s*[,}]", txt))
+    for k, v in opts.items():
+        assert getattr(L, "OPT_" + k) == v, k
+    for k, v in algos.items():
+        assert getattr(L, "ALGO_" + k) == v, k
+    ctx = L.ddp_create(numels("toy"), L.FP32, 4096, 2, 0)
+    try:
+        for k, v in opts.items():
+            L.ddp_get_option(ctx, v)                 # every key is known to the library
+        for a in algos.values():
+            L.ddp_set_option(ctx, L.OPT_ALGO, a)
+            assert L.ddp_get_option(ctx, L.OPT_ALGO) == a
+    finally:
+        L.ddp_destroy(ctx)
