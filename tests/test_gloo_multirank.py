@@ -122,8 +122,8 @@ def _worker_unused(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_two_ranks_unused_and_rebuilt_map_agree():
-    world = 2
+@pytest.mark.parametrize("world", [2, 4])
+def test_ranks_unused_and_rebuilt_map_agree(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -135,7 +135,7 @@ def test_two_ranks_unused_and_rebuilt_map_agree():
         p.join(timeout=60)
         assert p.exitcode == 0
     gathered = res[0][1]
-    (s0, m0), (s1, m1) = gathered
-    nb = len(s0[0])
-    assert all(seq == list(range(nb)) for seq in s0 + s1)   # same launch sequence on both ranks
-    assert m0 == m1                                           # same rebuilt map on both ranks
+    nb = len(gathered[0][0][0])
+    for seqs, _ in gathered:
+        assert all(seq == list(range(nb)) for seq in seqs)   # same launch sequence on every rank
+    assert all(m == gathered[0][1] for _, m in gathered)      # same rebuilt map on every rank
