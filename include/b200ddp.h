@@ -67,17 +67,20 @@ typedef enum {
 enum {
   DDP_OPT_OVERLAP = 1,          /* 1 (default): launch buckets from the hooks; 0: launch all at
                                    finalize — the non-overlapped baseline of P:L164-L175 / L399 */
-  DDP_OPT_P2P_ONESHOT_MAX = 2,  /* buckets <= this many bytes use the one-shot P2P kernel */
-  DDP_OPT_P2P_TWOSHOT_MAX = 3,  /* buckets <= this many bytes use the two-shot P2P kernel; larger
-                                   buckets use NCCL */
-  DDP_OPT_COMM_CTAS = 4,        /* max CTAs of a P2P kernel when world > 1 (1..148, default 32) */
+  DDP_OPT_P2P_ONESHOT_MAX = 2,  /* buckets <= this many bytes use the one-shot P2P kernel (default
+                                   1 MiB); larger ones the world-dependent default (world 2: CE,
+                                   world > 2: two-shot) */
+  DDP_OPT_P2P_TWOSHOT_MAX = 3,  /* buckets larger than this many bytes use NCCL (default: none) */
+  DDP_OPT_COMM_CTAS = 4,        /* max CTAs of a P2P kernel when world > 1 (1..148, default 32);
+                                   the last bucket of a pass always runs on 148 */
   DDP_OPT_DRY_RUN = 5,          /* 1: protocol only, no device work (host tests; CREATED only) */
   DDP_OPT_PROFILE = 6,          /* 1: time every device launch with CUDA events */
   DDP_OPT_ALGO = 7,             /* force the bucket allreduce: 0 auto, 1 NCCL, 2 one-shot, 3 two-shot,
                                    4 copy-engine one-shot (world > 1), 5 NVLS (needs MULTICAST),
                                    6 SM push + stream-ordered reduce, 7 copy-engine two-shot,
                                    8 stream-ordered NVLS (world > 1) */
-  DDP_OPT_PACK_CTAS = 8,        /* max CTAs of pack/unpack kernels and of P2P kernels at world 1 */
+  DDP_OPT_PACK_CTAS = 8,        /* max CTAs of the HBM-bound kernels (pack, unpack, CE gather /
+                                   reduce, world-1 fused kernel); 1..9472, default 4736 */
   DDP_OPT_P2P_STAGE_BYTES = 9,  /* 0 (default): one pipeline stage per CTA chunk; else split each
                                    CTA chunk into stages of this many bytes (one sync per stage) */
   DDP_OPT_FIND_UNUSED = 10,     /* 1: globally-unused-parameter detection:
