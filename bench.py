@@ -56,8 +56,8 @@ def parse():
     ap.add_argument("--ce-streams", type=int, default=0)
     ap.add_argument("--throughput-policy", action="store_true",
                     help="exposed-time runs: DDP without the overlap policy (PREFER_OVERLAP=0)")
-    ap.add_argument("--overlap-policy", action="store_true",
-                    help="exposed-time runs: force the overlap policy (PREFER_OVERLAP=1), e.g. for bf16")
+    ap.add_argument("--overlap-policy", type=int, default=-1,
+                    help="force PREFER_OVERLAP (1 copy engines, 2 SM kernels) for the DDP / exposed runs")
     ap.add_argument("--high-priority", action="store_true",
                     help="communication streams at the highest priority (default: lowest)")
     ap.add_argument("--lanes", type=int, default=0, help="P2P/NVLS kernel lanes (streams)")
@@ -230,8 +230,8 @@ def run_ours(a):
         opts[L.OPT_CE_STREAMS] = a.ce_streams
     if a.throughput_policy:
         opts[L.OPT_PREFER_OVERLAP] = 0
-    if a.overlap_policy:
-        opts[L.OPT_PREFER_OVERLAP] = 1
+    if a.overlap_policy >= 0:
+        opts[L.OPT_PREFER_OVERLAP] = a.overlap_policy
     if a.high_priority:
         opts[L.OPT_LOW_PRIORITY] = 0
     if a.lanes:
@@ -725,8 +725,8 @@ def _opts(a):
         o[L.OPT_CE_STREAMS] = a.ce_streams
     if a.throughput_policy:
         o[L.OPT_PREFER_OVERLAP] = 0
-    if a.overlap_policy:
-        o[L.OPT_PREFER_OVERLAP] = 1
+    if a.overlap_policy >= 0:
+        o[L.OPT_PREFER_OVERLAP] = a.overlap_policy
     if a.high_priority:
         o[L.OPT_LOW_PRIORITY] = 0
     if a.lanes:

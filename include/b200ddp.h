@@ -112,10 +112,12 @@ enum {
                                    round-robin) are created at the lowest priority, so queued backward
                                    kernels are scheduled first; 0: highest.  Before binding only */
   DDP_OPT_PREFER_OVERLAP = 18   /* automatic policy for gradients produced by a running backward
-                                   (the front end's DistributedDataParallel sets it): at world > 2
-                                   every bucket but the last uses the SM-free copy-engine two-shot
-                                   (CE2), the last one the fastest kernel on every SM.  Default 0:
+                                   (the front end's DistributedDataParallel sets it).  0 (default):
                                    the policy that is fastest when all buckets are ready at once.
+                                   1 (copy engines; chosen for fp32): at world > 2 every bucket but
+                                   the last uses the SM-free copy-engine two-shot (CE2), the last one
+                                   the fastest kernel on every SM.  2 (SM kernels; chosen for bf16):
+                                   at world 2 the one-shot kernel instead of the copy engines.
                                    Layout key */
 };
 

@@ -105,7 +105,10 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
     // two-shot keeps the SMs with autograd (lowest exposed time at W=4,
     // profiles/r01_n4.md); the last bucket overlaps nothing and keeps the
     // fastest kernel on every SM
-    if (c->prefer_overlap && c->world > 2 && &bk != &c->buckets.back()) a = DDP_ALGO_CE2;
+    if (c->prefer_overlap == 1 && c->world > 2 && &bk != &c->buckets.back()) a = DDP_ALGO_CE2;
+    // PREFER_OVERLAP=2 (SM kernels under backward): at world 2 the one-shot kernel
+    // instead of the copy engines — measured better for bf16 models (profiles/r01_n2.md)
+    if (c->prefer_overlap == 2 && c->world == 2) a = DDP_ALGO_ONESHOT;
   } else {
     a = DDP_ALGO_NCCL;
   }
@@ -777,7 +780,8 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       c->ce_direct = v;
       break;
     case DDP_OPT_PREFER_OVERLAP:
-      c->prefer_overlap = v ? 1 : 0;
+      if (v < 0 || v > 2) return fail(DDP_ERR_INVALID_ARG, "PREFER_OVERLAP must be 0, 1 or 2");
+      c->prefer_overlap = v;
       break;
     case DDP_OPT_LOW_PRIORITY:
       if (c->bound) return fail(DDP_ERR_STATE, "LOW_PRIORITY is fixed once bound");

@@ -221,13 +221,13 @@ class DistributedDataParallel(torch.nn.Module):
         options = dict(options or {})
         if find_unused_parameters:
             options[L.OPT_FIND_UNUSED] = 1
-        # DDP's buckets are synced while backward still runs: the overlap policy
-        # (SM-free exchanges except for the last bucket) unless the caller chose.
-        # Measured at W=4 (profiles/r01_n4.md): it cuts BERT-large fp32's exposed
-        # time 8.7% -> 5.3%, but with bf16 gradients (a backward half as long) the
-        # copy engines fall behind (9.4% -> 17-31%), so bf16 keeps the kernels
+        # DDP's buckets are synced while backward still runs, so an overlap policy
+        # applies unless the caller chose.  Measured (profiles/r01_n2.md, r01_n4.md):
+        # fp32 models hide the exchange best with the copy engines (BERT-large W=4
+        # 8.7% -> 4.3% exposed), bf16 models — a backward half as long — with the SM
+        # kernels (W=2: CE 10.6-11.6% vs one-shot 6.7%; W=4: CE2 15-31% vs two-shot 8.8%)
         dtypes_ = {p.dtype for p in module.parameters() if p.requires_grad}
-        options.setdefault(L.OPT_PREFER_OVERLAP, 1 if dtypes_ == {torch.float32} else 0)
+        options.setdefault(L.OPT_PREFER_OVERLAP, 1 if dtypes_ == {torch.float32} else 2)
         self.module = module
         self.params = [p for p in module.parameters() if p.requires_grad]
         dtypes = {p.dtype for p in self.params}
