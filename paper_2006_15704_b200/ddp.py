@@ -207,6 +207,9 @@ class DistributedDataParallel(torch.nn.Module):
     ``rebuild_buckets``: gradient order prediction — after the
     first synced backward, rank 0's traced ready order is broadcast and the
     parameter-to-bucket map is rebuilt from it once, at the next forward.
+    The exchange policy for hook-driven passes is ``DDP_OPT_PREFER_OVERLAP``:
+    1 (copy engines) for fp32 models, 2 (SM kernels) otherwise, unless
+    ``options`` sets it.
     """
 
     def __init__(self, module: torch.nn.Module, process_group=None, bucket_cap_mb: float = 25,
