@@ -156,3 +156,25 @@ def test_explicit_order_brute_force_and_invariants():
         assert _params_per_bucket(d) == _params_per_bucket(assign_buckets(ns, esize, cap))
     with pytest.raises(ValueError):
         assign_buckets([1, 2, 3], 4, 10, [0, 0, 1])
+
+
+try:
+    from hypothesis import given, settings
+    from hypothesis import strategies as st
+except ImportError:  # pragma: no cover
+    given = None
+
+if given is not None:
+    @settings(max_examples=300, deadline=None)
+    @given(ns=st.lists(st.integers(1, 64), min_size=1, max_size=10),
+           esize=st.sampled_from([1, 2, 4]), cap=st.integers(0, 400), seed=st.integers(0, 10 ** 6))
+    def test_property_assignment_matches_longest_prefix(ns, esize, cap, seed):
+        """Property: for any sizes, cap and scan order, the greedy map equals the
+        longest-prefix formulation and tiles every bucket exactly."""
+        order = list(range(len(ns)))
+        random.Random(seed).shuffle(order)
+        a = assign_buckets(ns, esize, cap, order)
+        assert _params_per_bucket(a) == _brute_force_order(ns, esize, cap, order)
+        for b, slots in enumerate(a.buckets):
+            assert [o for _, o in slots] == list(itertools.accumulate([0] + [ns[p] for p, _ in slots[:-1]]))
+            assert a.bucket_numel[b] == sum(ns[p] for p, _ in slots)
