@@ -62,6 +62,8 @@ def parse():
                     help="communication streams at the highest priority (default: lowest)")
     ap.add_argument("--lanes", type=int, default=0, help="P2P/NVLS kernel lanes (streams)")
     ap.add_argument("--wire-bf16", action="store_true", help="N-3: fp32 gradients travel as bf16 (CE exchange)")
+    ap.add_argument("--grad-view", action="store_true",
+                    help="N-3 zero-copy: gradients live in their bucket slots (in-place NCCL, no pack/unpack)")
     ap.add_argument("--ce-direct-mib", type=float, default=-1, help="CE: copy gradients >= this straight from .grad")
     ap.add_argument("--nccl-comms", type=int, default=0, help="round-robin NCCL communicators (P:L535)")
     ap.add_argument("--exposed-model", default="resnet50", choices=["none", "resnet50", "bert_large"],
@@ -238,6 +240,8 @@ def run_ours(a):
         opts[L.OPT_LANES] = a.lanes
     if a.wire_bf16:
         opts[L.OPT_WIRE_BF16] = 1
+    if a.grad_view:
+        opts[L.OPT_GRAD_VIEW] = 1
     if a.ce_direct_mib >= 0:
         opts[L.OPT_CE_DIRECT_BYTES] = int(a.ce_direct_mib * MIB)
     if a.nccl_comms:
@@ -255,6 +259,9 @@ def run_ours(a):
         pos += (n * esize + 255) // 256 * 256 // esize
     flat = torch.empty(pos, dtype=tdt, device=dev)
     grads = [flat[o:o + n] for o, n in zip(offs, ns)]
+    if a.grad_view:  # each gradient IS its bucket slot (ddp_param_storage_offset)
+        grads = [red._storage[o:o + n * esize].view(tdt)
+                 for o, n in ((L.ddp_param_storage_offset(red.ctx, p), n) for p, n in enumerate(ns))]
     sdev.fill_all(grads, 15704, rank, 0, "normal", a.dtype)
     order = list(range(len(ns) - 1, -1, -1))
     batch = L.ReadyBatch(order, [grads[p].data_ptr() for p in order])
@@ -563,9 +570,15 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
     ddp = DistributedDataParallel(model, bucket_cap_mb=cap_mib, options=opts)
     stream = torch.cuda.current_stream(dev)
 
-    def one(sync: bool) -> float:
+    def clear_grads():
         for p in ddp.params:
-            p.grad = None
+            if ddp.gradient_as_bucket_view and p.grad is not None:
+                p.grad.zero_()          # keeps the bucket views (zero_grad(set_to_none=False))
+            else:
+                p.grad = None
+
+    def one(sync: bool) -> float:
+        clear_grads()
         loss = fwd(ddp)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if sync:
@@ -583,8 +596,7 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
     def group(n: int, sync_last: bool = True) -> float:
         """n-1 accumulating no_sync backward passes + 1 synced one (sync_last) or n
         no_sync ones (the baseline with the same .grad accumulation): summed backward ms."""
-        for p in ddp.params:
-            p.grad = None
+        clear_grads()
         tot = 0.0
         for k in range(n):
             loss = fwd(ddp)
@@ -733,6 +745,8 @@ def _opts(a):
         o[L.OPT_LANES] = a.lanes
     if a.wire_bf16:
         o[L.OPT_WIRE_BF16] = 1
+    if a.grad_view:
+        o[L.OPT_GRAD_VIEW] = 1
     if a.ce_direct_mib >= 0:
         o[L.OPT_CE_DIRECT_BYTES] = int(a.ce_direct_mib * MIB)
     if a.nccl_comms:

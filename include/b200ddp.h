@@ -111,7 +111,7 @@ enum {
   DDP_OPT_LOW_PRIORITY = 17,    /* 1 (default): the library's own streams (lanes, copy-engine,
                                    round-robin) are created at the lowest priority, so queued backward
                                    kernels are scheduled first; 0: highest.  Before binding only */
-  DDP_OPT_PREFER_OVERLAP = 18   /* automatic policy for gradients produced by a running backward
+  DDP_OPT_PREFER_OVERLAP = 18,  /* automatic policy for gradients produced by a running backward
                                    (the front end's DistributedDataParallel sets it).  0 (default):
                                    the policy that is fastest when all buckets are ready at once.
                                    1 (copy engines; chosen for fp32): at world > 2 every bucket but
@@ -119,10 +119,21 @@ enum {
                                    the fastest kernel on every SM.  2 (SM kernels; chosen for bf16):
                                    at world 2 the one-shot kernel instead of the copy engines.
                                    Layout key */
+  DDP_OPT_GRAD_VIEW = 19        /* gradient-as-bucket-view (§8(f) N-3, zero-copy variant; the
+                                   paper's buckets hold copies, Alg. 1 L231-L232 / L246): 1 = the
+                                   caller places each gradient AT its bucket slot in this rank's
+                                   storage (ddp_param_storage_offset), so a3 and a6 vanish: every
+                                   bucket uses DDP_ALGO_NCCL, an in-place ncclAllReduce with
+                                   ncclAvg (each operand x fl(1/W), then the sum — oracle O-3b up
+                                   to NCCL's summation order).  A gradient passed at any other
+                                   address is still correct: it is copied raw into its slot before
+                                   and back after the allreduce.  Not combinable with FIND_UNUSED
+                                   or WIRE_BF16 (DDP_ERR_UNSUPPORTED).  Default 0; layout key */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.
- *   NCCL:    pack kernel -> ncclAllReduce(sum) -> unpack kernel
+ *   NCCL:    pack kernel -> ncclAllReduce(sum) -> unpack kernel (DDP_OPT_GRAD_VIEW: in-place
+ *            ncclAllReduce(avg) on the slots the gradients live in; no pack / unpack)
  *   ONESHOT: one fused sm_100a kernel: pack, push to every peer, rank-order reduce into .grad
  *   TWOSHOT: one fused sm_100a kernel: pack + reduce-scatter push, reduce, all-gather push, unpack
  *   CE:      pack kernel -> copy-engine pushes (cudaMemcpyAsync over NVLink) ordered by stream
@@ -179,6 +190,11 @@ ddp_status_t ddp_param_location(const ddp_ctx_t* ctx, int32_t p, int32_t* bucket
 ddp_status_t ddp_storage_bytes(const ddp_ctx_t* ctx, int64_t* bytes);
 /* Allreduce algorithm chosen for bucket b (DDP_ALGO_*), given current options. */
 ddp_status_t ddp_bucket_algo(const ddp_ctx_t* ctx, int32_t b, int32_t* algo);
+/* Byte offset, inside this rank's storage, of parameter p's bucket slot: its
+ * gradient (param_numel[p] elements of the context dtype, contiguous) lives
+ * there under DDP_OPT_GRAD_VIEW.  Depends on options: query after
+ * ddp_set_option.  Errors: DDP_ERR_INVALID_ARG (NULL / bad index). */
+ddp_status_t ddp_param_storage_offset(const ddp_ctx_t* ctx, int32_t p, int64_t* byte_offset);
 
 /* ---- device binding (once; collective across ranks) ---------------------
  * ddp_get_nccl_id: rank 0 creates the NCCL unique id (128 bytes); the caller

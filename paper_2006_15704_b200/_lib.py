@@ -25,7 +25,7 @@ FP32, BF16 = 0, 1
 OPT_OVERLAP, OPT_P2P_ONESHOT_MAX, OPT_P2P_TWOSHOT_MAX, OPT_COMM_CTAS, OPT_DRY_RUN, OPT_PROFILE, \
     OPT_ALGO, OPT_PACK_CTAS, OPT_P2P_STAGE_BYTES, OPT_FIND_UNUSED, OPT_MULTICAST, OPT_CE_STREAMS, \
     OPT_NCCL_COMMS, OPT_CE_DIRECT_BYTES, OPT_WIRE_BF16, OPT_LANES, OPT_LOW_PRIORITY, \
-    OPT_PREFER_OVERLAP = range(1, 19)
+    OPT_PREFER_OVERLAP, OPT_GRAD_VIEW = range(1, 20)
 ALGO_AUTO, ALGO_NCCL, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_CE, ALGO_NVLS, ALGO_PUSH, ALGO_CE2, ALGO_NVLS2 = range(9)
 ALGO_NAMES = {ALGO_NCCL: "nccl", ALGO_ONESHOT: "oneshot", ALGO_TWOSHOT: "twoshot", ALGO_CE: "ce",
               ALGO_NVLS: "nvls", ALGO_PUSH: "push", ALGO_CE2: "ce2", ALGO_NVLS2: "nvls2"}
@@ -54,6 +54,7 @@ _SIGS = {
     "ddp_bucket_slot": (C.c_int, [_P, C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
     "ddp_param_location": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]),
     "ddp_storage_bytes": (C.c_int, [_P, C.POINTER(C.c_int64)]),
+    "ddp_param_storage_offset": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int64)]),
     "ddp_bucket_algo": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32)]),
     "ddp_get_nccl_id": (C.c_int, [C.c_char_p]),
     "ddp_bind_device": (C.c_int, [_P, C.c_int32, C.c_char_p, _P, C.POINTER(_P), _P]),
@@ -155,6 +156,12 @@ def ddp_param_location(ctx: int, p: int) -> Tuple[int, int]:
     b, o = C.c_int32(), C.c_int64()
     _check(lib().ddp_param_location(ctx, p, C.byref(b), C.byref(o)))
     return b.value, o.value
+
+
+def ddp_param_storage_offset(ctx: int, p: int) -> int:
+    v = C.c_int64()
+    _check(lib().ddp_param_storage_offset(ctx, p, C.byref(v)))
+    return v.value
 
 
 def ddp_storage_bytes(ctx: int) -> int:

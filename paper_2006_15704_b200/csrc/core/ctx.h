@@ -92,6 +92,7 @@ struct ddp_ctx {
           low_priority = 1;  // library streams at the lowest priority: backward's kernels first
                              // (measured: exposed 3.1 -> 2.8% at W=2, 9.3 -> 9.0% at W=4)
   int64_t prefer_overlap = 0;  // policy for buckets synced under a running backward (see resolve_algo)
+  int64_t grad_view = 0;       // N-3 zero-copy: gradients live in their bucket slots (NCCL in place)
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
           stage1_stride = 0, ce_flags_off = 0, bitmap_off = 0, scratch_off = 0, storage_bytes = 0;

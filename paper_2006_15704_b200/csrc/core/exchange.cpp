@@ -270,6 +270,45 @@ ddp_status_t launch_nvls2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
   return DDP_OK;
 }
 
+// Gradient-as-bucket-view (N-3, zero-copy): the gradients normally ARE the
+// bucket's slots, so pack (Alg. 1) and the copy back (L246) vanish and
+// the bucket is averaged in place: ncclAvg multiplies every operand by fl(1/W)
+// before summing (oracle O-3b up to NCCL's summation order).  A gradient handed
+// over at another address (e.g. .grad re-created after zero_grad(set_to_none))
+// is copied raw into its slot first and the average copied back after, per
+// maximal run of such slots.
+ddp_status_t launch_nccl_view(ddp_ctx* c, const Bucket& bk, char* buf, ncclComm_t comm, cudaStream_t s) {
+  const int n = (int)bk.params.size();
+  std::vector<std::pair<int, int>> runs;  // [k0, k1) of slots not at their slot address
+  for (int k = 0; k < n;) {
+    if (bk.grads[k] == buf + bk.off[k] * c->esize) {
+      ++k;
+      continue;
+    }
+    int e = k;
+    while (e < n && bk.grads[e] != buf + bk.off[e] * c->esize) ++e;
+    runs.emplace_back(k, e);
+    k = e;
+  }
+  if (!runs.empty()) prof_begin(c, 0, s);
+  for (auto& r : runs) {
+    const SlotView sv{bk.off.data() + r.first, bk.grads.data() + r.first, r.second - r.first};
+    CUDA_TRY(c, launch_pack(c->dtype, sv, buf, 1.0f, (int)c->pack_ctas, s));
+  }
+  if (!runs.empty()) prof_end(c, s);
+  prof_begin(c, 1, s);
+  NCCL_TRY(c, ncclAllReduce(buf, buf, (size_t)bk.numel, c->dtype == DDP_FP32 ? ncclFloat32 : ncclBfloat16,
+                            ncclAvg, comm, s));
+  prof_end(c, s);
+  if (!runs.empty()) prof_begin(c, 2, s);
+  for (auto& r : runs) {
+    const SlotView sv{bk.off.data() + r.first, bk.grads.data() + r.first, r.second - r.first};
+    CUDA_TRY(c, launch_unpack(c->dtype, sv, buf, (int)c->pack_ctas, s));
+  }
+  if (!runs.empty()) prof_end(c, s);
+  return DDP_OK;
+}
+
 // ---- a3/a4/a6 device work for one bucket -------------------------------------
 ddp_status_t launch_device(ddp_ctx* c, int b) {
   Bucket& bk = c->buckets[b];
@@ -285,6 +324,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
     cudaStream_t s = k == 0 ? c->comm : c->rr_stream[k];
     ncclComm_t comm = k == 0 ? c->nccl : c->rr_comm[k];
     if (k) c->rr_used[k] = 1;
+    if (c->grad_view) return launch_nccl_view(c, bk, static_cast<char*>(buf), comm, s);
     prof_begin(c, 0, s);
     CUDA_TRY(c, launch_pack(c->dtype, sv, buf, scale, (int)c->pack_ctas, s));
     prof_end(c, s);

@@ -78,6 +78,7 @@ void assign(ddp_ctx* c) {
 
 int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   const int64_t bytes = bk.numel * c->esize;
+  if (c->grad_view) return DDP_ALGO_NCCL;  // in place on the slots the gradients live in
   int a;
   if (c->algo != DDP_ALGO_AUTO) {
     a = (int)c->algo;
@@ -313,7 +314,7 @@ ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s, b
 bool is_layout_key(int32_t k) {
   return k == DDP_OPT_P2P_ONESHOT_MAX || k == DDP_OPT_P2P_TWOSHOT_MAX || k == DDP_OPT_ALGO ||
          k == DDP_OPT_FIND_UNUSED || k == DDP_OPT_MULTICAST || k == DDP_OPT_CE_DIRECT_BYTES ||
-         k == DDP_OPT_WIRE_BF16 || k == DDP_OPT_LANES || k == DDP_OPT_PREFER_OVERLAP;
+         k == DDP_OPT_WIRE_BF16 || k == DDP_OPT_LANES || k == DDP_OPT_PREFER_OVERLAP || k == DDP_OPT_GRAD_VIEW;
 }
 
 }  // namespace
@@ -455,6 +456,12 @@ ddp_status_t ddp_param_location(const ddp_ctx_t* c, int32_t p, int32_t* bucket, 
   if (!c || p < 0 || p >= (int32_t)c->numel.size()) return fail(DDP_ERR_INVALID_ARG, "bad param");
   if (bucket) *bucket = c->p_bucket[p];
   if (offset) *offset = c->p_off[p];
+  return DDP_OK;
+}
+
+ddp_status_t ddp_param_storage_offset(const ddp_ctx_t* c, int32_t p, int64_t* byte_offset) {
+  if (!c || !byte_offset || p < 0 || p >= (int32_t)c->numel.size()) return fail(DDP_ERR_INVALID_ARG, "bad param");
+  *byte_offset = c->buckets[c->p_bucket[p]].byte_off + c->p_off[p] * c->esize;
   return DDP_OK;
 }
 
@@ -770,7 +777,13 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       c->algo = v;
       break;
     case DDP_OPT_FIND_UNUSED:
+      if (v && c->grad_view) return fail(DDP_ERR_UNSUPPORTED, "FIND_UNUSED with GRAD_VIEW");
       c->find_unused = v ? 1 : 0;
+      break;
+    case DDP_OPT_GRAD_VIEW:
+      if (v && (c->find_unused || c->wire_bf16))
+        return fail(DDP_ERR_UNSUPPORTED, "GRAD_VIEW with FIND_UNUSED or WIRE_BF16");
+      c->grad_view = v ? 1 : 0;
       break;
     case DDP_OPT_MULTICAST:
       c->multicast = v ? 1 : 0;
@@ -793,6 +806,7 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       break;
     case DDP_OPT_WIRE_BF16:
       if (v && c->dtype != DDP_FP32) return fail(DDP_ERR_INVALID_ARG, "WIRE_BF16 compresses fp32 gradients only");
+      if (v && c->grad_view) return fail(DDP_ERR_UNSUPPORTED, "WIRE_BF16 with GRAD_VIEW");
       c->wire_bf16 = v ? 1 : 0;
       break;
     case DDP_OPT_NCCL_COMMS:
@@ -848,6 +862,7 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_LANES: *v = c->lanes; break;
     case DDP_OPT_LOW_PRIORITY: *v = c->low_priority; break;
     case DDP_OPT_PREFER_OVERLAP: *v = c->prefer_overlap; break;
+    case DDP_OPT_GRAD_VIEW: *v = c->grad_view; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;

@@ -207,6 +207,12 @@ class DistributedDataParallel(torch.nn.Module):
     ``rebuild_buckets``: gradient order prediction — after the
     first synced backward, rank 0's traced ready order is broadcast and the
     parameter-to-bucket map is rebuilt from it once, at the next forward.
+    ``gradient_as_bucket_view`` (§8(f) N-3, zero-copy): after the first synced
+    backward every ``.grad`` is a view of its bucket slot in the library's
+    storage, so the buckets are averaged in place (``DDP_OPT_GRAD_VIEW``: no
+    pack / unpack).  Clear gradients with ``zero_grad(set_to_none=False)`` to
+    keep the views; a re-created ``.grad`` is copied into its slot and the view
+    re-attached at the end of the pass.
     The exchange policy for hook-driven passes is ``DDP_OPT_PREFER_OVERLAP``:
     1 (copy engines) for fp32 models, 2 (SM kernels) otherwise, unless
     ``options`` sets it.
@@ -214,8 +220,13 @@ class DistributedDataParallel(torch.nn.Module):
 
     def __init__(self, module: torch.nn.Module, process_group=None, bucket_cap_mb: float = 25,
                  broadcast_parameters: bool = True, options: Optional[Dict[int, int]] = None,
-                 find_unused_parameters: bool = False, rebuild_buckets: bool = False):
+                 find_unused_parameters: bool = False, rebuild_buckets: bool = False,
+                 gradient_as_bucket_view: bool = False):
         super().__init__()
+        if gradient_as_bucket_view and find_unused_parameters:
+            raise ValueError("gradient_as_bucket_view with find_unused_parameters is not supported")
+        gradient_as_bucket_view = gradient_as_bucket_view or bool((options or {}).get(L.OPT_GRAD_VIEW))
+        self.gradient_as_bucket_view = gradient_as_bucket_view
         self.find_unused_parameters = find_unused_parameters
         self.process_group = process_group
         self.bucket_cap_mb = bucket_cap_mb
@@ -224,6 +235,8 @@ class DistributedDataParallel(torch.nn.Module):
         options = dict(options or {})
         if find_unused_parameters:
             options[L.OPT_FIND_UNUSED] = 1
+        if gradient_as_bucket_view:
+            options[L.OPT_GRAD_VIEW] = 1
         # DDP's buckets are synced while backward still runs, so an overlap policy
         # applies unless the caller chose.  Measured (profiles/r01_n2.md, r01_n4.md):
         # fp32 models hide the exchange best with the copy engines (BERT-large W=4
@@ -241,6 +254,7 @@ class DistributedDataParallel(torch.nn.Module):
         self.reducer = GradReducer([p.numel() for p in self.params], self._dtype,
                                    int(bucket_cap_mb * MIB), group=process_group,
                                    device=self.params[0].device, options=options)
+        self._views = self._make_views()
         if broadcast_parameters and self.reducer.world > 1:
             states = [t for t in list(module.parameters()) + list(module.buffers()) if t.is_contiguous()]
             with torch.no_grad():
@@ -251,6 +265,17 @@ class DistributedDataParallel(torch.nn.Module):
         self._param_index = {id(p): i for i, p in enumerate(self.params)}
         self._hooks = [p.register_post_accumulate_grad_hook(self._make_hook(i))
                        for i, p in enumerate(self.params)]
+
+    def _make_views(self) -> Optional[List[torch.Tensor]]:
+        """Each parameter's bucket slot in this rank's storage, shaped like the
+        parameter (DDP_OPT_GRAD_VIEW; ddp_param_storage_offset)."""
+        if not self.gradient_as_bucket_view:
+            return None
+        st, views = self.reducer._storage, []
+        for i, p in enumerate(self.params):
+            o = L.ddp_param_storage_offset(self.reducer.ctx, i)
+            views.append(st[o:o + p.numel() * p.element_size()].view(p.dtype).view(p.shape))
+        return views
 
     def _make_hook(self, idx: int):
         def hook(p: torch.Tensor):
@@ -267,6 +292,11 @@ class DistributedDataParallel(torch.nn.Module):
     def _finalize(self):
         self._pass_open = False
         self.reducer.finalize()
+        if self._views is not None and not self._in_no_sync:
+            # the slots hold the averages of every gradient (in place): attach them
+            for p, v in zip(self.params, self._views):
+                if p.grad is not None and p.grad.data_ptr() != v.data_ptr():
+                    p.grad = v
         if self._rebuild and not self._in_no_sync:
             self._rebuild = False
             order = torch.tensor(self.reducer.ready_order(), dtype=torch.int32, device=self.params[0].device)
@@ -292,6 +322,7 @@ class DistributedDataParallel(torch.nn.Module):
         self.reducer = GradReducer([p.numel() for p in self.params], self._dtype,
                                    int(self.bucket_cap_mb * MIB), group=self.process_group,
                                    device=self.params[0].device, options=self._options, scan_order=order)
+        self._views = self._make_views()
 
     def forward(self, *args, **kwargs):
         if self._new_order is not None:

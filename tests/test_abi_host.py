@@ -381,3 +381,53 @@ def test_option_and_algo_constants_match_header():
             assert L.ddp_get_option(ctx, L.OPT_ALGO) == a
     finally:
         L.ddp_destroy(ctx)
+
+
+@pytest.mark.parametrize("model,esize", [("resnet50", 4), ("bert_large", 2), ("toy", 4)])
+def test_grad_view_layout(model, esize):
+    """DDP_OPT_GRAD_VIEW (N-3 zero-copy): every bucket is averaged in place by
+    NCCL; each parameter's slot (ddp_param_storage_offset) sits at its bucket's
+    base + its element offset (O-1 mapping), inside the storage, slots disjoint
+    and in the same order as the oracle's buckets."""
+    ns = numels(model)
+    cap = 25 * MIB
+    ctx = L.ddp_create(ns, L.FP32 if esize == 4 else L.BF16, cap, 4, 1)
+    try:
+        L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_TWOSHOT)     # GRAD_VIEW overrides it
+        L.ddp_set_option(ctx, L.OPT_GRAD_VIEW, 1)
+        assert L.ddp_get_option(ctx, L.OPT_GRAD_VIEW) == 1
+        nb = L.ddp_num_buckets(ctx)
+        assert {L.ddp_bucket_algo(ctx, b) for b in range(nb)} == {L.ALGO_NCCL}
+        total = L.ddp_storage_bytes(ctx)
+        a = assign_buckets(ns, esize, cap)
+        spans = []
+        for b, slots in enumerate(a.buckets):
+            base = None
+            for p, off in slots:
+                o = L.ddp_param_storage_offset(ctx, p)
+                bb, eo = L.ddp_param_location(ctx, p)
+                assert bb == b and eo == off
+                base = o - eo * esize if base is None else base
+                assert o == base + off * esize and base % 256 == 0
+                assert 0 <= o and o + ns[p] * esize <= total
+                spans.append((o, o + ns[p] * esize))
+        spans.sort()
+        assert all(x[1] <= y[0] for x, y in zip(spans, spans[1:]))
+        # not combinable with the options that need their own copies
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_set_option(ctx, L.OPT_FIND_UNUSED, 1)
+        assert e.value.status == L.ERR_UNSUPPORTED
+        if esize == 4:
+            with pytest.raises(L.DDPError) as e:
+                L.ddp_set_option(ctx, L.OPT_WIRE_BF16, 1)
+            assert e.value.status == L.ERR_UNSUPPORTED
+        with pytest.raises(L.DDPError):
+            L.ddp_param_storage_offset(ctx, len(ns))
+        L.ddp_set_option(ctx, L.OPT_GRAD_VIEW, 0)
+        assert {L.ddp_bucket_algo(ctx, b) for b in range(nb)} == {L.ALGO_TWOSHOT}
+        L.ddp_set_option(ctx, L.OPT_FIND_UNUSED, 1)
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_set_option(ctx, L.OPT_GRAD_VIEW, 1)
+        assert e.value.status == L.ERR_UNSUPPORTED
+    finally:
+        L.ddp_destroy(ctx)
