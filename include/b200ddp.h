@@ -122,10 +122,13 @@ enum {
   DDP_OPT_GRAD_VIEW = 19        /* gradient-as-bucket-view (§8(f) N-3, zero-copy variant; the
                                    paper's buckets hold copies, Alg. 1 L231-L232 / L246): 1 = the
                                    caller places each gradient AT its bucket slot in this rank's
-                                   storage (ddp_param_storage_offset), so a3 and a6 vanish: every
-                                   bucket uses DDP_ALGO_NCCL, an in-place ncclAllReduce with
-                                   ncclAvg (each operand x fl(1/W), then the sum — oracle O-3b up
-                                   to NCCL's summation order).  A gradient passed at any other
+                                   storage (ddp_param_storage_offset), so a3 and a6 vanish.  At
+                                   world 2 every bucket uses DDP_ALGO_CE (unless DDP_OPT_ALGO forces
+                                   NCCL): the bucket region travels as one copy-engine transfer per
+                                   peer and the rank-order reduce writes back in place (O-3b,
+                                   bit-exact).  Otherwise DDP_ALGO_NCCL: an in-place ncclAllReduce
+                                   with ncclAvg (each operand x fl(1/W), then the sum — O-3b up to
+                                   NCCL's summation order).  A gradient passed at any other
                                    address is still correct: it is copied raw into its slot before
                                    and back after the allreduce.  Not combinable with FIND_UNUSED
                                    or WIRE_BF16 (DDP_ERR_UNSUPPORTED).  Default 0; layout key */

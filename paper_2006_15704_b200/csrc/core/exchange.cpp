@@ -60,8 +60,11 @@ ddp_status_t ce_wait(ddp_ctx* c, cudaStream_t s, uint32_t* addr, uint32_t v) {
 //   comm stream:    [wait: peers consumed pass v-1] -> copies -> ready flags to peers
 //   reduce stream:  [wait: own copies issued, peers' ready flags] -> rank-order
 //                   reduce x 1/W per operand straight into .grad -> consumed flags
+ddp_status_t launch_ce_view(ddp_ctx* c, int b);
+
 ddp_status_t launch_ce(ddp_ctx* c, int b) {
   Bucket& bk = c->buckets[b];
+  if (c->grad_view) return launch_ce_view(c, b);
   const int W = c->world, r = c->rank;
   char* mine = static_cast<char*>(c->storage[r]);
   char* own_slot = mine + bk.ce_off + r * bk.ce_stride;
@@ -149,6 +152,72 @@ ddp_status_t launch_ce(ddp_ctx* c, int b) {
     const int j = (r + i) % W;
     if (ddp_status_t st = ce_write(c, c->ce_red, ce_flag(c, j, 1, b, r), v)) return st;
   }
+  c->ce_used = true;
+  return DDP_OK;
+}
+
+// Copy-engine one-shot with gradient-as-bucket-view (N-3 zero-copy): the
+// gradients are the bucket region, so the gather disappears, the whole region
+// travels as ONE copy per peer into slot r (wire layout = bucket layout) and
+// the rank-order reduce (x 1/W per operand, O-3b) writes back into the region
+// as one flat range.  Gradients handed over elsewhere are packed raw into the
+// region first (comm stream) and unpacked after the reduce (reduce stream).
+// Ordering as launch_ce: consumed flags guard slot reuse, ready flags the
+// reduce, and the reduce follows this rank's own copies out of the region.
+ddp_status_t launch_ce_view(ddp_ctx* c, int b) {
+  Bucket& bk = c->buckets[b];
+  const int W = c->world, r = c->rank;
+  char* mine = static_cast<char*>(c->storage[r]);
+  char* region = mine + bk.byte_off;
+  const uint32_t v = ++bk.ce_count;
+  const int n = (int)bk.params.size();
+  std::vector<std::pair<int, int>> runs;  // [k0, k1) of slots not at their slot address
+  for (int k = 0; k < n;) {
+    if (bk.grads[k] == region + bk.off[k] * c->esize) {
+      ++k;
+      continue;
+    }
+    int e = k;
+    while (e < n && bk.grads[e] != region + bk.off[e] * c->esize) ++e;
+    runs.emplace_back(k, e);
+    k = e;
+  }
+  if (!runs.empty()) prof_begin(c, 0, c->comm);
+  for (auto& q : runs) {
+    const SlotView sv{bk.off.data() + q.first, bk.grads.data() + q.first, q.second - q.first};
+    CUDA_TRY(c, launch_pack(c->dtype, sv, region, 1.0f, (int)c->pack_ctas, c->comm));
+  }
+  if (!runs.empty()) prof_end(c, c->comm);
+  if (v > 1)
+    for (int i = 1; i < W; ++i)
+      if (ddp_status_t st = ce_wait(c, c->comm, ce_flag(c, r, 1, b, (r + i) % W), v - 1)) return st;
+  prof_begin(c, 4);
+  for (int i = 1; i < W; ++i) {
+    char* dst = static_cast<char*>(c->storage[(r + i) % W]) + bk.ce_off + r * bk.ce_stride;
+    CUDA_TRY(c, cudaMemcpyAsync(dst, region, (size_t)(bk.numel * c->esize), cudaMemcpyDeviceToDevice, c->comm));
+  }
+  prof_end(c);
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_write(c, c->comm, ce_flag(c, (r + i) % W, 0, b, r), v)) return st;
+  CUDA_TRY(c, cudaEventRecord(c->ce_copied[b], c->comm));
+  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_red, c->ce_copied[b], 0));
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_wait(c, c->ce_red, ce_flag(c, r, 0, b, (r + i) % W), v)) return st;
+  void* flat[1] = {region};
+  const int64_t wire0[1] = {0}, numel[1] = {bk.numel};
+  const CeView rv{flat, wire0, numel, 1};
+  prof_begin(c, 5, c->ce_red);
+  CUDA_TRY(c, launch_ce_reduce(c->dtype, W, r, rv, mine + bk.ce_off, bk.ce_stride, 1.0f / (float)W,
+                               (int)c->pack_ctas, c->ce_red));
+  prof_end(c, c->ce_red);
+  for (int i = 1; i < W; ++i)
+    if (ddp_status_t st = ce_write(c, c->ce_red, ce_flag(c, (r + i) % W, 1, b, r), v)) return st;
+  if (!runs.empty()) prof_begin(c, 2, c->ce_red);
+  for (auto& q : runs) {
+    const SlotView sv{bk.off.data() + q.first, bk.grads.data() + q.first, q.second - q.first};
+    CUDA_TRY(c, launch_unpack(c->dtype, sv, region, (int)c->pack_ctas, c->ce_red));
+  }
+  if (!runs.empty()) prof_end(c, c->ce_red);
   c->ce_used = true;
   return DDP_OK;
 }

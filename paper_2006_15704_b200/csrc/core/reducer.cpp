@@ -78,7 +78,10 @@ void assign(ddp_ctx* c) {
 
 int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   const int64_t bytes = bk.numel * c->esize;
-  if (c->grad_view) return DDP_ALGO_NCCL;  // in place on the slots the gradients live in
+  // gradient-as-bucket-view: in place on the slots the gradients live in — the
+  // copy-engine exchange at world 2 (unless NCCL is forced), NCCL otherwise
+  if (c->grad_view)
+    return c->world == 2 && (c->algo == DDP_ALGO_AUTO || c->algo == DDP_ALGO_CE) ? DDP_ALGO_CE : DDP_ALGO_NCCL;
   int a;
   if (c->algo != DDP_ALGO_AUTO) {
     a = (int)c->algo;
@@ -193,6 +196,15 @@ void plan(ddp_ctx* c) {
     const size_t ns = bk.params.size();
     bk.ce_wire.assign(ns, 0);
     bk.ce_direct.assign(ns, 0);
+    if (c->grad_view) {  // wire layout = bucket layout: the bucket region travels as one copy
+      for (size_t k = 0; k < ns; ++k) bk.ce_wire[k] = bk.off[k];
+      bk.ce_small0 = 0;
+      bk.ce_wire_numel = bk.numel;
+      bk.ce_stride = align_up(bk.numel * c->esize, 256);
+      bk.ce_off = pos;
+      pos += c->world * bk.ce_stride;
+      continue;
+    }
     int64_t w = 0;
     for (int pass = 0; pass < 2; ++pass) {  // direct gradients first, then the small ones
       if (pass == 1) bk.ce_small0 = w;

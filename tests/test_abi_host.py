@@ -425,6 +425,16 @@ def test_grad_view_layout(model, esize):
             L.ddp_param_storage_offset(ctx, len(ns))
         L.ddp_set_option(ctx, L.OPT_GRAD_VIEW, 0)
         assert {L.ddp_bucket_algo(ctx, b) for b in range(nb)} == {L.ALGO_TWOSHOT}
+        # world 2: the copy-engine exchange in place, unless NCCL is forced
+        two = L.ddp_create(ns, L.FP32 if esize == 4 else L.BF16, cap, 2, 0)
+        try:
+            L.ddp_set_option(two, L.OPT_GRAD_VIEW, 1)
+            assert {L.ddp_bucket_algo(two, b) for b in range(nb)} == {L.ALGO_CE}
+            assert L.ddp_storage_bytes(two) >= 3 * sum(ns) * esize   # bucket region + 2 CE slots
+            L.ddp_set_option(two, L.OPT_ALGO, L.ALGO_NCCL)
+            assert {L.ddp_bucket_algo(two, b) for b in range(nb)} == {L.ALGO_NCCL}
+        finally:
+            L.ddp_destroy(two)
         L.ddp_set_option(ctx, L.OPT_FIND_UNUSED, 1)
         with pytest.raises(L.DDPError) as e:
             L.ddp_set_option(ctx, L.OPT_GRAD_VIEW, 1)

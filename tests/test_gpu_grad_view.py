@@ -3,7 +3,8 @@ DDP_OPT_GRAD_VIEW) through the front end and the C ABI: after the first synced
 backward every ``.grad`` is its bucket slot in the library's storage, the
 buckets are averaged in place (no pack / unpack launches) and the result is
 the average of the ranks' local gradients — oracle O-3 (Alg. 1
-L231-L238) within the NCCL tolerance of test_gpu_multigpu (world 2), identity
+L231-L238): bit-exact O-3b with the copy-engine exchange (world 2 default),
+within the NCCL tolerance of test_gpu_multigpu when NCCL is forced, identity
 at world 1 (C-12)."""
 
 import os
@@ -14,7 +15,7 @@ import pytest
 import torch
 import torch.multiprocessing as mp
 
-from oracle.average import average_fp64
+from oracle.average import average_bitfaithful, average_fp64
 
 pytestmark = pytest.mark.gpu
 
@@ -86,7 +87,7 @@ def test_world1_grad_view():
         ddp.close()
 
 
-def _worker(rank, world, init_file, q):
+def _worker(rank, world, init_file, q, opts=None):
     torch.cuda.set_device(rank)
     import torch.distributed as dist
     dist.init_process_group("nccl", init_method=f"file://{init_file}", rank=rank, world_size=world,
@@ -97,7 +98,7 @@ def _worker(rank, world, init_file, q):
         torch.manual_seed(11)
         m = _Mlp().cuda()
         ddp = DistributedDataParallel(m, bucket_cap_mb=0.01, gradient_as_bucket_view=True,
-                                      options={L.OPT_PROFILE: 1})
+                                      options={L.OPT_PROFILE: 1, **(opts or {})})
         local = _Mlp().cuda()
         local.load_state_dict(m.state_dict())
         torch.manual_seed(50 + rank)                    # different data on every rank
@@ -111,16 +112,14 @@ def _worker(rank, world, init_file, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.multigpu
-@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-def test_world2_grad_view():
+def _run2(opts=None):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     fd, init_file = tempfile.mkstemp(prefix="b200ddp_gv_")
     os.close(fd)
     os.unlink(init_file)
-    ps = [ctx.Process(target=_worker, args=(r, world, init_file, q)) for r in range(world)]
+    ps = [ctx.Process(target=_worker, args=(r, world, init_file, q, opts)) for r in range(world)]
     for p in ps:
         p.start()
     try:
@@ -132,7 +131,39 @@ def test_world2_grad_view():
                 p.kill()
     for r, _, _, err in res:
         assert err is None, f"rank {r}: {err}"
-    assert set(res[0][2]) == {"nccl"} and len(res[0][2]) > 1
+    return res
+
+
+def _check_views(res, world=2):
+    for r in range(world):
+        for it in range(3):
+            _, _, npack, nunpack, views = res[r][1][it]
+            assert views
+            assert (npack > 0) if it == 0 else (npack == 0 and nunpack == 0), (it, r, npack, nunpack)
+
+
+@pytest.mark.multigpu
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_world2_grad_view_ce():
+    world = 2
+    res = _run2()
+    _check_views(res)
+    assert set(res[0][2]) == {"ce"} and len(res[0][2]) > 1      # world 2: copy engines, in place
+    for it in range(3):
+        for k in range(len(res[0][1][it][0])):
+            want = average_bitfaithful([res[r][1][it][1][k].ravel() for r in range(world)], "fp32")
+            for r in range(world):
+                assert np.array_equal(res[r][1][it][0][k].ravel(), want), (it, k, r)   # O-3b, bit-exact
+
+
+@pytest.mark.multigpu
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_world2_grad_view_nccl():
+    from paper_2006_15704_b200 import _lib as L
+    world = 2
+    res = _run2({L.OPT_ALGO: L.ALGO_NCCL})
+    _check_views(res)
+    assert set(res[0][2]) == {"nccl"}
     for it in range(3):
         for k in range(len(res[0][1][it][0])):
             ref, den = average_fp64([res[r][1][it][1][k].ravel() for r in range(world)], "fp32")
@@ -141,7 +172,3 @@ def test_world2_grad_view():
                 assert np.array_equal(got, res[0][1][it][0][k].ravel())     # replicas identical
                 y = got.astype(np.float64)
                 assert np.all(np.abs(y - ref.astype(np.float64)) <= 1e-6 * den + 1e-45), (it, k, r)
-        for r in range(world):
-            _, _, npack, nunpack, views = res[r][1][it]
-            assert views
-            assert (npack > 0) if it == 0 else (npack == 0 and nunpack == 0), (it, r, npack, nunpack)
