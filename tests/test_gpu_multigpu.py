@@ -53,6 +53,10 @@ def _worker(rank, world, init_file, cfgs, q):
             ns = numels(model)
             red = GradReducer(ns, dtype, cap, options={L.OPT_ALGO: algo, **(cfg[5] if len(cfg) > 5 else {})})
             grads = [torch.empty(n, dtype=TDT[dtype], device="cuda") for n in ns]
+            if len(cfg) > 5 and cfg[5].get(L.OPT_GRAD_VIEW):   # N-3 zero-copy: grads ARE the slots
+                es = 4 if dtype == "fp32" else 2
+                grads = [red._storage[o:o + n * es].view(TDT[dtype])
+                         for o, n in ((L.ddp_param_storage_offset(red.ctx, p), n) for p, n in enumerate(ns))]
             idx = [torch.from_numpy(_sample_idx(p, n)).cuda() for p, n in enumerate(ns)]
             res = []
             for it in range(iters):
@@ -119,7 +123,11 @@ def test_multigpu_parity(world):
             ("bert_large", "bf16", 25 * MIB, L.ALGO_CE2, 1),
             ("resnet50", "fp32", 5 * MIB, L.ALGO_AUTO, 2, {L.OPT_PREFER_OVERLAP: 1}),
             ("bert_large", "fp32", 25 * MIB, L.ALGO_AUTO, 1),      # the bench's BERT config as launched
-            ("toy", "fp32", 4096, L.ALGO_NVLS2, 2), ("resnet50", "bf16", 25 * MIB, L.ALGO_NVLS2, 2)]
+            ("toy", "fp32", 4096, L.ALGO_NVLS2, 2), ("resnet50", "bf16", 25 * MIB, L.ALGO_NVLS2, 2),
+            # gradient-as-bucket-view (N-3): CE in place at W=2 (bit-exact), NCCL in place otherwise
+            ("resnet50", "fp32", 25 * MIB, L.ALGO_AUTO, 2, {L.OPT_GRAD_VIEW: 1}),
+            ("bert_large", "bf16", 25 * MIB, L.ALGO_AUTO, 1, {L.OPT_GRAD_VIEW: 1}),
+            ("toy", "fp32", 4096, L.ALGO_NCCL, 2, {L.OPT_GRAD_VIEW: 1})]
     outs = _run(world, cfgs)
     for ci, cfg in enumerate(cfgs):
         model, dtype, cap, algo, iters = cfg[:5]
@@ -127,6 +135,8 @@ def test_multigpu_parity(world):
         algos = outs[0][ci][1]
         tol = any(x in ("nccl", "nvls", "nvls2") for x in algos)   # not rank-order sums: tolerance parity
         wire = len(cfg) > 5 and cfg[5].get(L.OPT_WIRE_BF16)
+        if len(cfg) > 5 and cfg[5].get(L.OPT_GRAD_VIEW) and algo == L.ALGO_AUTO:
+            assert set(algos) == ({"ce"} if world == 2 else {"nccl"}), algos
         for it in range(iters):
             for p in range(len(ns)):
                 sums = [outs[r][ci][0][it][0][p] for r in range(world)]
