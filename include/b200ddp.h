@@ -122,13 +122,15 @@ enum {
   DDP_OPT_GRAD_VIEW = 19        /* gradient-as-bucket-view (§8(f) N-3, zero-copy variant; the
                                    paper's buckets hold copies, Alg. 1 L231-L232 / L246): 1 = the
                                    caller places each gradient AT its bucket slot in this rank's
-                                   storage (ddp_param_storage_offset), so a3 and a6 vanish.  At
-                                   world 2 every bucket uses DDP_ALGO_CE (unless DDP_OPT_ALGO forces
-                                   NCCL): the bucket region travels as one copy-engine transfer per
-                                   peer and the rank-order reduce writes back in place (O-3b,
-                                   bit-exact).  Otherwise DDP_ALGO_NCCL: an in-place ncclAllReduce
-                                   with ncclAvg (each operand x fl(1/W), then the sum — O-3b up to
-                                   NCCL's summation order).  A gradient passed at any other
+                                   storage (ddp_param_storage_offset), so a3 and a6 vanish.  Every
+                                   bucket uses DDP_ALGO_CE at world 2 (the bucket region travels as
+                                   one copy-engine transfer per peer, the rank-order reduce writes
+                                   back in place) and DDP_ALGO_CE2 wider (reduce-scatter copies of
+                                   the raw region, each operand x fl(1/W) in the shard reduce,
+                                   all-gather into the peers' regions): O-3b, bit-exact.  With
+                                   DDP_OPT_ALGO = NCCL, or at world 1: an in-place ncclAllReduce with
+                                   ncclAvg (each operand x fl(1/W), then the sum — O-3b up to NCCL's
+                                   summation order).  A gradient passed at any other
                                    address is still correct: it is copied raw into its slot before
                                    and back after the allreduce.  Not combinable with FIND_UNUSED
                                    or WIRE_BF16 (DDP_ERR_UNSUPPORTED).  Default 0; layout key */

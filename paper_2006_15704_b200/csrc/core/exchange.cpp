@@ -62,6 +62,38 @@ ddp_status_t ce_wait(ddp_ctx* c, cudaStream_t s, uint32_t* addr, uint32_t v) {
 //                   reduce x 1/W per operand straight into .grad -> consumed flags
 ddp_status_t launch_ce_view(ddp_ctx* c, int b);
 
+// Gradient-as-bucket-view: maximal runs [k0, k1) of the bucket's slots whose
+// gradient was handed over somewhere else than its slot in `region`.
+std::vector<std::pair<int, int>> alias_runs(const ddp_ctx* c, const Bucket& bk, const char* region) {
+  const int n = (int)bk.params.size();
+  std::vector<std::pair<int, int>> runs;
+  for (int k = 0; k < n;) {
+    if (bk.grads[k] == region + bk.off[k] * c->esize) {
+      ++k;
+      continue;
+    }
+    int e = k;
+    while (e < n && bk.grads[e] != region + bk.off[e] * c->esize) ++e;
+    runs.emplace_back(k, e);
+    k = e;
+  }
+  return runs;
+}
+
+// raw copies of those runs into the region (before) / back out of it (after)
+ddp_status_t copy_runs(ddp_ctx* c, const Bucket& bk, const std::vector<std::pair<int, int>>& runs, char* region,
+                       bool in, cudaStream_t s) {
+  if (runs.empty()) return DDP_OK;
+  prof_begin(c, in ? 0 : 2, s);
+  for (auto& q : runs) {
+    const SlotView sv{bk.off.data() + q.first, bk.grads.data() + q.first, q.second - q.first};
+    if (in) CUDA_TRY(c, launch_pack(c->dtype, sv, region, 1.0f, (int)c->pack_ctas, s));
+    else CUDA_TRY(c, launch_unpack(c->dtype, sv, region, (int)c->pack_ctas, s));
+  }
+  prof_end(c, s);
+  return DDP_OK;
+}
+
 ddp_status_t launch_ce(ddp_ctx* c, int b) {
   Bucket& bk = c->buckets[b];
   if (c->grad_view) return launch_ce_view(c, b);
@@ -170,24 +202,8 @@ ddp_status_t launch_ce_view(ddp_ctx* c, int b) {
   char* mine = static_cast<char*>(c->storage[r]);
   char* region = mine + bk.byte_off;
   const uint32_t v = ++bk.ce_count;
-  const int n = (int)bk.params.size();
-  std::vector<std::pair<int, int>> runs;  // [k0, k1) of slots not at their slot address
-  for (int k = 0; k < n;) {
-    if (bk.grads[k] == region + bk.off[k] * c->esize) {
-      ++k;
-      continue;
-    }
-    int e = k;
-    while (e < n && bk.grads[e] != region + bk.off[e] * c->esize) ++e;
-    runs.emplace_back(k, e);
-    k = e;
-  }
-  if (!runs.empty()) prof_begin(c, 0, c->comm);
-  for (auto& q : runs) {
-    const SlotView sv{bk.off.data() + q.first, bk.grads.data() + q.first, q.second - q.first};
-    CUDA_TRY(c, launch_pack(c->dtype, sv, region, 1.0f, (int)c->pack_ctas, c->comm));
-  }
-  if (!runs.empty()) prof_end(c, c->comm);
+  const auto runs = alias_runs(c, bk, region);
+  if (ddp_status_t st = copy_runs(c, bk, runs, region, true, c->comm)) return st;
   if (v > 1)
     for (int i = 1; i < W; ++i)
       if (ddp_status_t st = ce_wait(c, c->comm, ce_flag(c, r, 1, b, (r + i) % W), v - 1)) return st;
@@ -212,12 +228,7 @@ ddp_status_t launch_ce_view(ddp_ctx* c, int b) {
   prof_end(c, c->ce_red);
   for (int i = 1; i < W; ++i)
     if (ddp_status_t st = ce_write(c, c->ce_red, ce_flag(c, (r + i) % W, 1, b, r), v)) return st;
-  if (!runs.empty()) prof_begin(c, 2, c->ce_red);
-  for (auto& q : runs) {
-    const SlotView sv{bk.off.data() + q.first, bk.grads.data() + q.first, q.second - q.first};
-    CUDA_TRY(c, launch_unpack(c->dtype, sv, region, (int)c->pack_ctas, c->ce_red));
-  }
-  if (!runs.empty()) prof_end(c, c->ce_red);
+  if (ddp_status_t st = copy_runs(c, bk, runs, region, false, c->ce_red)) return st;
   c->ce_used = true;
   return DDP_OK;
 }
@@ -245,9 +256,19 @@ ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
   const int64_t L = bk.shard, e = c->esize;
   const int64_t half = (int64_t)(v & 1) * W * bk.ce_stride;
   auto shard_len = [&](int j) { return std::max<int64_t>(0, std::min<int64_t>(L, bk.numel - j * L)); };
-  prof_begin(c, 0, c->ce_pack);
-  CUDA_TRY(c, launch_pack(c->dtype, sv, own, scale, (int)c->pack_ctas, c->ce_pack));
-  prof_end(c, c->ce_pack);
+  // gradient-as-bucket-view: the gradients are the bucket region, so no pack /
+  // unpack (only raw copies for gradients handed over elsewhere); the reduce
+  // scales every operand instead (O-3b).  The all-gather from peer j writes
+  // only shard j, which this rank's reduce-scatter copy has already sent to j.
+  const bool view = c->grad_view != 0;
+  const auto runs = view ? alias_runs(c, bk, own) : std::vector<std::pair<int, int>>();
+  if (view) {
+    if (ddp_status_t st = copy_runs(c, bk, runs, own, true, c->ce_pack)) return st;
+  } else {
+    prof_begin(c, 0, c->ce_pack);
+    CUDA_TRY(c, launch_pack(c->dtype, sv, own, scale, (int)c->pack_ctas, c->ce_pack));
+    prof_end(c, c->ce_pack);
+  }
   CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
   // reduce-scatter on the CE2 copy stream(s); each transfer is followed by its peer's flag
   const size_t nst = c->ce2_rs.size();
@@ -271,7 +292,8 @@ ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
     src[q] = q == r ? static_cast<const void*>(own + r * L * e)
                     : static_cast<const void*>(mine + bk.ce_off + half + q * bk.ce_stride);
   prof_begin(c, 5, c->ce_red);
-  CUDA_TRY(c, launch_shard_reduce(c->dtype, W, src, own + r * L * e, shard_len(r), (int)c->pack_ctas, c->ce_red));
+  CUDA_TRY(c, launch_shard_reduce(c->dtype, W, src, own + r * L * e, shard_len(r), view ? scale : 1.0f,
+                                  (int)c->pack_ctas, c->ce_red));
   prof_end(c, c->ce_red);
   CUDA_TRY(c, cudaEventRecord(c->ce_reduced[b], c->ce_red));
   // all-gather the reduced own shard into every peer's bucket
@@ -290,9 +312,13 @@ ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
   CUDA_TRY(c, cudaStreamWaitEvent(c->ce_up, c->ce_reduced[b], 0));
   for (int i = 1; i < W; ++i)
     if (ddp_status_t st = ce_wait(c, c->ce_up, ce_flag(c, r, 2, b, (r + i) % W), v)) return st;
-  prof_begin(c, 2, c->ce_up);
-  CUDA_TRY(c, launch_unpack(c->dtype, sv, own, (int)c->pack_ctas, c->ce_up));
-  prof_end(c, c->ce_up);
+  if (view) {
+    if (ddp_status_t st = copy_runs(c, bk, runs, own, false, c->ce_up)) return st;
+  } else {
+    prof_begin(c, 2, c->ce_up);
+    CUDA_TRY(c, launch_unpack(c->dtype, sv, own, (int)c->pack_ctas, c->ce_up));
+    prof_end(c, c->ce_up);
+  }
   c->ce2_used = true;
   return DDP_OK;
 }
@@ -347,35 +373,13 @@ ddp_status_t launch_nvls2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
 // is copied raw into its slot first and the average copied back after, per
 // maximal run of such slots.
 ddp_status_t launch_nccl_view(ddp_ctx* c, const Bucket& bk, char* buf, ncclComm_t comm, cudaStream_t s) {
-  const int n = (int)bk.params.size();
-  std::vector<std::pair<int, int>> runs;  // [k0, k1) of slots not at their slot address
-  for (int k = 0; k < n;) {
-    if (bk.grads[k] == buf + bk.off[k] * c->esize) {
-      ++k;
-      continue;
-    }
-    int e = k;
-    while (e < n && bk.grads[e] != buf + bk.off[e] * c->esize) ++e;
-    runs.emplace_back(k, e);
-    k = e;
-  }
-  if (!runs.empty()) prof_begin(c, 0, s);
-  for (auto& r : runs) {
-    const SlotView sv{bk.off.data() + r.first, bk.grads.data() + r.first, r.second - r.first};
-    CUDA_TRY(c, launch_pack(c->dtype, sv, buf, 1.0f, (int)c->pack_ctas, s));
-  }
-  if (!runs.empty()) prof_end(c, s);
+  const auto runs = alias_runs(c, bk, buf);
+  if (ddp_status_t st = copy_runs(c, bk, runs, buf, true, s)) return st;
   prof_begin(c, 1, s);
   NCCL_TRY(c, ncclAllReduce(buf, buf, (size_t)bk.numel, c->dtype == DDP_FP32 ? ncclFloat32 : ncclBfloat16,
                             ncclAvg, comm, s));
   prof_end(c, s);
-  if (!runs.empty()) prof_begin(c, 2, s);
-  for (auto& r : runs) {
-    const SlotView sv{bk.off.data() + r.first, bk.grads.data() + r.first, r.second - r.first};
-    CUDA_TRY(c, launch_unpack(c->dtype, sv, buf, (int)c->pack_ctas, s));
-  }
-  if (!runs.empty()) prof_end(c, s);
-  return DDP_OK;
+  return copy_runs(c, bk, runs, buf, false, s);
 }
 
 // ---- a3/a4/a6 device work for one bucket -------------------------------------

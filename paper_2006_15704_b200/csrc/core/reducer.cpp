@@ -79,9 +79,13 @@ void assign(ddp_ctx* c) {
 int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   const int64_t bytes = bk.numel * c->esize;
   // gradient-as-bucket-view: in place on the slots the gradients live in — the
-  // copy-engine exchange at world 2 (unless NCCL is forced), NCCL otherwise
-  if (c->grad_view)
-    return c->world == 2 && (c->algo == DDP_ALGO_AUTO || c->algo == DDP_ALGO_CE) ? DDP_ALGO_CE : DDP_ALGO_NCCL;
+  // copy-engine exchanges (one-shot CE at world 2, two-shot CE2 wider) unless
+  // NCCL is forced; NCCL at world 1
+  if (c->grad_view) {
+    if (c->world == 1 || c->algo == DDP_ALGO_NCCL) return DDP_ALGO_NCCL;
+    if (c->algo == DDP_ALGO_CE || c->algo == DDP_ALGO_CE2) return (int)c->algo;
+    return c->world == 2 ? DDP_ALGO_CE : DDP_ALGO_CE2;
+  }
   int a;
   if (c->algo != DDP_ALGO_AUTO) {
     a = (int)c->algo;

@@ -76,9 +76,10 @@ struct CeView {
 };
 // own_slot[wire_k + i] = grad_k[i] (raw) for the listed (small) gradients.
 cudaError_t launch_ce_gather(int dtype, const CeView& v, void* own_slot, int max_ctas, cudaStream_t s);
-// CE2: dst[i] = RNE(sum_q src_q[i]) in rank order q = 0..world-1 (fp32 accumulate).
-cudaError_t launch_shard_reduce(int dtype, int world, const void* const* src, void* dst, int64_t n, int max_ctas,
-                                cudaStream_t s);
+// CE2: dst[i] = RNE(sum_q src_q[i]) in rank order q = 0..world-1 (fp32 accumulate);
+// scale != 1: every operand scaled and rounded first, RNE(sum_q RNE(src_q[i] * scale)).
+cudaError_t launch_shard_reduce(int dtype, int world, const void* const* src, void* dst, int64_t n, float scale,
+                                int max_ctas, cudaStream_t s);
 // SM push: every listed gradient (raw) to peer_slots[j] + wire_k, j < npeers.
 cudaError_t launch_ce_push(int dtype, const CeView& v, void* const* peer_slots, int npeers, int max_ctas,
                            cudaStream_t s);

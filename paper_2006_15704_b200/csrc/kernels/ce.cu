@@ -223,13 +223,14 @@ cudaError_t push_by_world(int npeers, const CeView& v, const PeerDst& pd, int ma
 
 // CE2: dst[i] = RNE( sum_{q<W} src_q[i] ), rank order, fp32 (the values are
 // pre-scaled by pack); dst may alias src_rank (same element, same thread).
+// EACH (gradient-as-bucket-view: raw operands): RNE( sum_q RNE(src_q[i] * s) ) = O-3b.
 struct ShardSrc {
   const void* p[kMaxWorld];
 };
 
-template <typename T, int W>
+template <typename T, int W, bool EACH>
 __global__ void __launch_bounds__(kThreads) shard_reduce_kernel(const __grid_constant__ ShardSrc ss,
-                                                                T* dst, int64_t n) {
+                                                                T* dst, int64_t n, float s) {
   constexpr int64_t tile = kTileBytes / sizeof(T);
   for (int64_t t = (int64_t)blockIdx.x * tile; t < n; t += (int64_t)gridDim.x * tile) {
     const int64_t m = min(tile, n - t);
@@ -237,22 +238,23 @@ __global__ void __launch_bounds__(kThreads) shard_reduce_kernel(const __grid_con
     const T* src[W];
 #pragma unroll
     for (int q = 0; q < W; ++q) src[q] = static_cast<const T*>(ss.p[q]) + t;
-    cta_xfer<T, W, 1, false, false>(d, src, m, 1.0f);
+    cta_xfer<T, W, 1, false, EACH, EACH>(d, src, m, s);
   }
 }
 
-template <typename T>
-cudaError_t shard_reduce(int world, const ShardSrc& ss, void* dst, int64_t n, int max_ctas, cudaStream_t st) {
+template <typename T, bool EACH>
+cudaError_t shard_reduce(int world, const ShardSrc& ss, void* dst, int64_t n, float s, int max_ctas,
+                         cudaStream_t st) {
   const int grid = grid_for(n, kTileBytes / sizeof(T), max_ctas);
   T* d = static_cast<T*>(dst);
   switch (world) {
-    case 2: shard_reduce_kernel<T, 2><<<grid, kThreads, 0, st>>>(ss, d, n); break;
-    case 3: shard_reduce_kernel<T, 3><<<grid, kThreads, 0, st>>>(ss, d, n); break;
-    case 4: shard_reduce_kernel<T, 4><<<grid, kThreads, 0, st>>>(ss, d, n); break;
-    case 5: shard_reduce_kernel<T, 5><<<grid, kThreads, 0, st>>>(ss, d, n); break;
-    case 6: shard_reduce_kernel<T, 6><<<grid, kThreads, 0, st>>>(ss, d, n); break;
-    case 7: shard_reduce_kernel<T, 7><<<grid, kThreads, 0, st>>>(ss, d, n); break;
-    case 8: shard_reduce_kernel<T, 8><<<grid, kThreads, 0, st>>>(ss, d, n); break;
+    case 2: shard_reduce_kernel<T, 2, EACH><<<grid, kThreads, 0, st>>>(ss, d, n, s); break;
+    case 3: shard_reduce_kernel<T, 3, EACH><<<grid, kThreads, 0, st>>>(ss, d, n, s); break;
+    case 4: shard_reduce_kernel<T, 4, EACH><<<grid, kThreads, 0, st>>>(ss, d, n, s); break;
+    case 5: shard_reduce_kernel<T, 5, EACH><<<grid, kThreads, 0, st>>>(ss, d, n, s); break;
+    case 6: shard_reduce_kernel<T, 6, EACH><<<grid, kThreads, 0, st>>>(ss, d, n, s); break;
+    case 7: shard_reduce_kernel<T, 7, EACH><<<grid, kThreads, 0, st>>>(ss, d, n, s); break;
+    case 8: shard_reduce_kernel<T, 8, EACH><<<grid, kThreads, 0, st>>>(ss, d, n, s); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -260,13 +262,16 @@ cudaError_t shard_reduce(int world, const ShardSrc& ss, void* dst, int64_t n, in
 
 }  // namespace
 
-cudaError_t launch_shard_reduce(int dtype, int world, const void* const* src, void* dst, int64_t n, int max_ctas,
-                                cudaStream_t s) {
+cudaError_t launch_shard_reduce(int dtype, int world, const void* const* src, void* dst, int64_t n, float scale,
+                                int max_ctas, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
   ShardSrc ss{};
   for (int q = 0; q < world && q < kMaxWorld; ++q) ss.p[q] = src[q];
-  return dtype == 0 ? shard_reduce<float>(world, ss, dst, n, max_ctas, s)
-                    : shard_reduce<__nv_bfloat16>(world, ss, dst, n, max_ctas, s);
+  if (scale != 1.0f)
+    return dtype == 0 ? shard_reduce<float, true>(world, ss, dst, n, scale, max_ctas, s)
+                      : shard_reduce<__nv_bfloat16, true>(world, ss, dst, n, scale, max_ctas, s);
+  return dtype == 0 ? shard_reduce<float, false>(world, ss, dst, n, 1.0f, max_ctas, s)
+                    : shard_reduce<__nv_bfloat16, false>(world, ss, dst, n, 1.0f, max_ctas, s);
 }
 
 cudaError_t launch_ce_push(int dtype, const CeView& v, void* const* peer_slots, int npeers, int max_ctas,

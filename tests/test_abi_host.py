@@ -385,8 +385,8 @@ def test_option_and_algo_constants_match_header():
 
 @pytest.mark.parametrize("model,esize", [("resnet50", 4), ("bert_large", 2), ("toy", 4)])
 def test_grad_view_layout(model, esize):
-    """DDP_OPT_GRAD_VIEW (N-3 zero-copy): every bucket is averaged in place by
-    NCCL; each parameter's slot (ddp_param_storage_offset) sits at its bucket's
+    """DDP_OPT_GRAD_VIEW (N-3 zero-copy): every bucket is averaged in place (CE
+    at world 2, CE2 wider, NCCL when forced or at world 1); each parameter's slot (ddp_param_storage_offset) sits at its bucket's
     base + its element offset (O-1 mapping), inside the storage, slots disjoint
     and in the same order as the oracle's buckets."""
     ns = numels(model)
@@ -397,7 +397,10 @@ def test_grad_view_layout(model, esize):
         L.ddp_set_option(ctx, L.OPT_GRAD_VIEW, 1)
         assert L.ddp_get_option(ctx, L.OPT_GRAD_VIEW) == 1
         nb = L.ddp_num_buckets(ctx)
+        assert {L.ddp_bucket_algo(ctx, b) for b in range(nb)} == {L.ALGO_CE2}   # world 4: CE2 in place
+        L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_NCCL)
         assert {L.ddp_bucket_algo(ctx, b) for b in range(nb)} == {L.ALGO_NCCL}
+        L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_TWOSHOT)
         total = L.ddp_storage_bytes(ctx)
         a = assign_buckets(ns, esize, cap)
         spans = []

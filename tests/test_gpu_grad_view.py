@@ -112,8 +112,7 @@ def _worker(rank, world, init_file, q, opts=None):
         dist.destroy_process_group()
 
 
-def _run2(opts=None):
-    world = 2
+def _run2(opts=None, world=2):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     fd, init_file = tempfile.mkstemp(prefix="b200ddp_gv_")
@@ -172,3 +171,36 @@ def test_world2_grad_view_nccl():
                 assert np.array_equal(got, res[0][1][it][0][k].ravel())     # replicas identical
                 y = got.astype(np.float64)
                 assert np.all(np.abs(y - ref.astype(np.float64)) <= 1e-6 * den + 1e-45), (it, k, r)
+
+
+@pytest.mark.multigpu
+@pytest.mark.skipif(NGPU < 4, reason="needs >= 4 GPUs")
+def test_world4_grad_view_ce2():
+    """World 4: the copy-engine two-shot in place (CE2), bit-exact vs O-3b,
+    front end (MLP) and C ABI at full ResNet-50 size (sampled outputs)."""
+    world = 4
+    res = _run2(world=world)
+    _check_views(res, world)
+    assert set(res[0][2]) == {"ce2"} and len(res[0][2]) > 1
+    for it in range(3):
+        for k in range(len(res[0][1][it][0])):
+            want = average_bitfaithful([res[r][1][it][1][k].ravel() for r in range(world)], "fp32")
+            for r in range(world):
+                assert np.array_equal(res[r][1][it][0][k].ravel(), want), (it, k, r)
+    from oracle.assignment import MIB
+    from paper_2006_15704_b200 import _lib as L
+    from synth.gen import gen_values
+    from synth.shapes import numels
+    from tests.test_gpu_multigpu import _run, _sample_idx
+    cfgs = [("resnet50", "fp32", 25 * MIB, L.ALGO_AUTO, 2, {L.OPT_GRAD_VIEW: 1}),
+            ("toy", "bf16", 4096, L.ALGO_AUTO, 2, {L.OPT_GRAD_VIEW: 1})]
+    outs = _run(world, cfgs)
+    for ci, (model, dtype, cap, algo, iters, _) in enumerate(cfgs):
+        ns = numels(model)
+        assert set(outs[0][ci][1]) == {"ce2"}
+        for it in range(iters):
+            for p in range(len(ns)):
+                assert len({outs[r][ci][0][it][0][p] for r in range(world)}) == 1, (model, p)
+                idx = _sample_idx(p, ns[p])
+                xs = [gen_values(15704, r, it, p, idx, "normal", dtype) for r in range(world)]
+                assert np.array_equal(outs[0][ci][0][it][1][p], average_bitfaithful(xs, dtype)), (model, it, p)

@@ -124,7 +124,7 @@ def test_multigpu_parity(world):
             ("resnet50", "fp32", 5 * MIB, L.ALGO_AUTO, 2, {L.OPT_PREFER_OVERLAP: 1}),
             ("bert_large", "fp32", 25 * MIB, L.ALGO_AUTO, 1),      # the bench's BERT config as launched
             ("toy", "fp32", 4096, L.ALGO_NVLS2, 2), ("resnet50", "bf16", 25 * MIB, L.ALGO_NVLS2, 2),
-            # gradient-as-bucket-view (N-3): CE in place at W=2 (bit-exact), NCCL in place otherwise
+            # gradient-as-bucket-view (N-3): CE in place at W=2, CE2 wider (bit-exact); NCCL when forced
             ("resnet50", "fp32", 25 * MIB, L.ALGO_AUTO, 2, {L.OPT_GRAD_VIEW: 1}),
             ("bert_large", "bf16", 25 * MIB, L.ALGO_AUTO, 1, {L.OPT_GRAD_VIEW: 1}),
             ("toy", "fp32", 4096, L.ALGO_NCCL, 2, {L.OPT_GRAD_VIEW: 1})]
@@ -136,7 +136,7 @@ def test_multigpu_parity(world):
         tol = any(x in ("nccl", "nvls", "nvls2") for x in algos)   # not rank-order sums: tolerance parity
         wire = len(cfg) > 5 and cfg[5].get(L.OPT_WIRE_BF16)
         if len(cfg) > 5 and cfg[5].get(L.OPT_GRAD_VIEW) and algo == L.ALGO_AUTO:
-            assert set(algos) == ({"ce"} if world == 2 else {"nccl"}), algos
+            assert set(algos) == ({"ce"} if world == 2 else {"ce2"}), algos
         for it in range(iters):
             for p in range(len(ns)):
                 sums = [outs[r][ci][0][it][0][p] for r in range(world)]
