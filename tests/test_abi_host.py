@@ -444,3 +444,25 @@ def test_grad_view_layout(model, esize):
         assert e.value.status == L.ERR_UNSUPPORTED
     finally:
         L.ddp_destroy(ctx)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_grad_view_protocol_unchanged(world):
+    """GRAD_VIEW changes only what a launched bucket does on the device, not the
+    protocol: the launch trace of random ready orders (dry run) is the oracle
+    replay O-2 of the O-1 map, as without the option (Alg. 1)."""
+    ns = numels("resnet50")
+    a = assign_buckets(ns, 4, 5 * MIB)
+    ctx = L.ddp_create(ns, L.FP32, 5 * MIB, world, world - 1)
+    L.ddp_set_option(ctx, L.OPT_GRAD_VIEW, 1)
+    L.ddp_set_option(ctx, L.OPT_DRY_RUN, 1)
+    rng = random.Random(29 + world)
+    try:
+        want = {1: L.ALGO_NCCL, 2: L.ALGO_CE, 4: L.ALGO_CE2}[world]
+        assert {L.ddp_bucket_algo(ctx, b) for b in range(L.ddp_num_buckets(ctx))} == {want}
+        for _ in range(10):
+            order = list(range(len(ns)))
+            rng.shuffle(order)
+            assert _run_pass(ctx, order) == replay(a, order)
+    finally:
+        L.ddp_destroy(ctx)
