@@ -195,9 +195,12 @@ ddp_status_t ddp_param_location(const ddp_ctx_t* ctx, int32_t p, int32_t* bucket
 ddp_status_t ddp_storage_bytes(const ddp_ctx_t* ctx, int64_t* bytes);
 /* Allreduce algorithm chosen for bucket b (DDP_ALGO_*), given current options. */
 ddp_status_t ddp_bucket_algo(const ddp_ctx_t* ctx, int32_t b, int32_t* algo);
-/* Byte offset, inside this rank's storage, of parameter p's bucket slot: its
+/* Byte offset, inside this rank's storage, of parameter p's bucket slot — the
+ * view `b_i.narrow(offset, var.size())` of Alg. 1: its
  * gradient (param_numel[p] elements of the context dtype, contiguous) lives
- * there under DDP_OPT_GRAD_VIEW.  Depends on options: query after
+ * there under DDP_OPT_GRAD_VIEW (§8(f) N-3, zero-copy).  The caller owns the
+ * storage (ddp_bind_device's peer_storage[rank]); the library only reads and
+ * writes it inside launched buckets.  Depends on options: query after
  * ddp_set_option.  Errors: DDP_ERR_INVALID_ARG (NULL / bad index). */
 ddp_status_t ddp_param_storage_offset(const ddp_ctx_t* ctx, int32_t p, int64_t* byte_offset);
 
