@@ -182,15 +182,16 @@ def run_reference(a):
     ns = numels(a.workload)
     W = max(1, world)
     r = time_sync(ns, a.dtype, int(a.cap_mib * MIB), W, seed=15704, gen_grads=gen_grads,
-                  max_iters=a.warmup + a.steps, budget_s=120.0)
+                  max_iters=a.steps, budget_s=120.0, warmup=a.warmup)
     ms = r["sec_per_iter"] * 1e3
     line = {
         "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms/iter", "n_gpus": W,
-        "steps": r["iters"], "warmup": 0, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+        "steps": r["iters"], "warmup": r["warmup"], "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32" if a.dtype == "fp32" else "bf16", "data": "synthetic",
         "config": {"workload": workload_name(a), "params": r["params"], "world_simulated": W},
         "cpu_baseline": {"value": ms, "unit": "ms/iter", "cores": r["cores"], "kind": "oracle",
-                         "sample": f"{r['iters']} full iterations of oracle.average.simulate_ddp_sync "
+                         "sample": f"{r['warmup']} untimed + {r['iters']} timed full iterations (median; at most "
+                                   f"--steps, within a 120 s budget) of oracle.average.simulate_ddp_sync "
                                    f"(pack x1/W, rank-order fp32 allreduce, unpack) over {W} in-memory replicas"},
         "e2e": {"value": ms, "unit": "ms/iter", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
