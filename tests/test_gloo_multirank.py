@@ -49,16 +49,25 @@ def _worker(rank, world, port, q):
         L.ddp_destroy(ctx)
         gathered = [None] * world
         dist.all_gather_object(gathered, seqs)
+        # gradient-as-bucket-view: the copy engines write a peer's slot at THIS
+        # rank's offsets, so every rank must derive the same slot layout
+        vctx = L.ddp_create(ns, L.FP32, 5 << 20, world, rank)
+        L.ddp_set_option(vctx, L.OPT_GRAD_VIEW, 1)
+        layout = ([L.ddp_param_storage_offset(vctx, p) for p in range(len(ns))], L.ddp_storage_bytes(vctx),
+                  [L.ddp_bucket_algo(vctx, b) for b in range(L.ddp_num_buckets(vctx))])
+        L.ddp_destroy(vctx)
+        layouts = [None] * world
+        dist.all_gather_object(layouts, layout)
         nid = L.ddp_get_nccl_id() if rank == 0 else None
         got = _broadcast_id(nid, rank, None, torch.device("cpu"))
         ids = [None] * world
         dist.all_gather_object(ids, got)
-        q.put((rank, gathered, ids, nid))
+        q.put((rank, gathered, ids, nid, layouts))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_ranks_agree_on_launch_order_and_nccl_id():
+def test_two_ranks_agree_on_launch_order_nccl_id_and_view_layout():
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -78,6 +87,12 @@ def test_two_ranks_agree_on_launch_order_and_nccl_id():
             assert seq == list(range(nb))         # 0,1,2,... on every rank, every pass
     ids = res[0][2]
     assert ids[0] == ids[1] == res[0][3] and len(ids[0]) == 128
+    layouts = res[0][4]
+    assert all(lay == layouts[0] for lay in layouts)          # identical slot layout on every rank
+    offs, total, algos = layouts[0]
+    from paper_2006_15704_b200 import _lib as L
+    assert set(algos) == {L.ALGO_CE}                         # world 2: the copy-engine exchange in place
+    assert len(set(offs)) == len(offs) and max(offs) < total
 
 
 def _worker_unused(rank, world, port, q):
