@@ -69,7 +69,7 @@ def parse():
     ap.add_argument("--exposed-model", default="resnet50", choices=["none", "resnet50", "bert_large"],
                     help="real-model backward for the exposed-time measurement")
     ap.add_argument("--exposed-batch", type=int, default=0)
-    ap.add_argument("--exposed-iters", type=int, default=10)
+    ap.add_argument("--exposed-iters", type=int, default=50)
     ap.add_argument("--timeline-detail", action="store_true", help="include per-launch timeline in the JSON")
     ap.add_argument("--oneshot-max", type=int, default=-1)
     ap.add_argument("--twoshot-max", type=int, default=-1)
@@ -369,7 +369,7 @@ def run_ours(a):
             for s_ in range(L.ddp_bucket_info(red.ctx, b)[1]):
                 p, _ = L.ddp_bucket_slot(red.ctx, b, s_)
                 small += ns[p] * esize if ns[p] * esize < L.ddp_get_option(red.ctx, L.OPT_CE_DIRECT_BYTES) else 0
-    by = {x: sum(n * esize for n, y in zip(bnumel, algos) if y == x) for x in ("nccl", "oneshot", "twoshot", "ce", "nvls", "push", "ce2", "nvls2")}
+    by = {x: sum(n * esize for n, y in zip(bnumel, algos) if y == x) for x in ("nccl", "oneshot", "twoshot", "ce", "nvls", "push", "ce2")}
 
     def kind_bytes(kind):
         """(algorithmic bytes per step, bound, rule) of one profile kind."""
@@ -378,13 +378,13 @@ def run_ours(a):
         if kind == "pack":
             if a.wire_bf16:
                 return 1.5 * by["ce"], "hbm", "fp32 read + bf16 write of every gradient (compressed wire)"
-            return (2 * (by["nccl"] + small + by["ce2"] + by["nvls2"]), "hbm",
-                    "2 x bytes packed (NCCL, CE2 and NVLS2 buckets; CE small gradients)")
+            return (2 * (by["nccl"] + small + by["ce2"]), "hbm",
+                    "2 x bytes packed (NCCL and CE2 buckets; CE small gradients)")
         if kind == "unpack":
-            return 2 * (by["nccl"] + by["ce2"] + by["nvls2"]), "hbm", "2 x bucket bytes"
+            return 2 * (by["nccl"] + by["ce2"]), "hbm", "2 x bucket bytes"
         if kind == "p2p_fused":
             return (by["oneshot"] * (world - 1) + by["twoshot"] * 2 * (world - 1) / world
-                    + (by["nvls"] + by["nvls2"]) * (1 + 1 / world), "nvlink",
+                    + by["nvls"] * (1 + 1 / world), "nvlink",
                     "NVLink bytes per direction: one-shot (W-1)S, two-shot 2(W-1)/W S, NVLS (1+1/W)S")
         if kind == "ce_copy":
             wf = 0.5 if a.wire_bf16 else 1.0   # the compressed wire carries bf16
@@ -420,30 +420,10 @@ def run_ours(a):
                                  "bound": x["bound"], "active_ms_per_step": kinds[k][2] / kprof_steps}
                              for k in kinds for x in [roof_of(k)]}
 
-    # ---- bucket allreduce bus bandwidth on a 25 MiB bucket (N > 1) ------------------
+    # ---- bucket allreduce bus bandwidth on a 25 MiB bucket (N > 1), every algorithm ----
     busbw = None
     if world > 1:
-        n25 = 25 * MIB // esize
-        red25 = GradReducer([n25], a.dtype, 25 * MIB, options=opts)
-        g25 = torch.empty(n25, dtype=tdt, device=dev)
-        sdev.fill(g25, 15704, rank, 0, 0, "normal", a.dtype)
-        L.ddp_set_option(red25.ctx, L.OPT_PROFILE, 1)
-
-        def s25():
-            red25.grad_ready(0, g25, stream)
-            red25.finalize(stream)
-        for _ in range(5):
-            s25()
-        red25.profile_read()
-        barrier()
-        timed(s25, 20)
-        p25 = red25.profile_read()
-        t = sum(v[0] for v in p25.values()) / 20   # whole sync of the bucket (pack+AR+unpack or fused)
-        t = max_over_ranks(t)
-        busbw = {"value": 25 * MIB / (t * 1e-3) * 2 * (world - 1) / world / 1e9, "unit": "GB/s",
-                 "bucket_mib": 25, "algo": red25.bucket_algos()[0], "ms": t,
-                 "includes": "pack x1/W + allreduce + unpack"}
-        red25.close()
+        busbw = busbw_suite(a, world, local, dev, opts, stream, flush_l2, barrier, max_over_ranks)
 
     # ---- e2e through the public API with host buffers --------------------------------
     e2e = None
@@ -479,11 +459,16 @@ def run_ours(a):
         exposed = measure_exposed(a, rank, world, local, dev, opts)
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        from oracle.cpu_baseline import time_sync
+        from oracle.cpu_baseline import cpu_model, time_sync, time_sync_threads
         from synth.gen import gen_grads
         r = time_sync(ns, a.dtype, cap, 1, seed=15704, gen_grads=gen_grads, max_iters=3, budget_s=30)
+        rt = time_sync_threads(ns, a.dtype, cap, 1, seed=15704, gen_grads=gen_grads, max_iters=3, budget_s=30)
         cpu = {"value": r["sec_per_iter"] * 1e3, "unit": "ms/iter", "cores": r["cores"], "kind": "oracle",
-               "sample": f"{r['iters']} full iterations of oracle simulate_ddp_sync on the same workload (W=1)"}
+               "sample": f"{r['iters']} full iterations of oracle simulate_ddp_sync on the same workload (W=1)",
+               "all_core": {"value": rt["sec_per_iter"] * 1e3, "unit": "ms/iter", "cores": rt["threads"],
+                            "sample": f"{rt['iters']} full iterations, {rt['threads']} threads each owning an "
+                                      "element range of every gradient (oracle.cpu_baseline.time_sync_threads)"},
+               "assign_ms": r["assign_s"] * 1e3, "cpu_model": cpu_model(), "os_cpu_count": os.cpu_count()}
 
     if rank == 0:
         line = {
@@ -511,6 +496,148 @@ def run_ours(a):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+class NvlinkCounter:
+    """Cumulative NVLink data bytes (TX, RX) of one GPU, summed over its links
+    (NVML field values NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX, KiB; payload
+    only, no protocol overhead).  read() -> (tx_bytes, rx_bytes) or None."""
+
+    def __init__(self, index: int):
+        self.h = None
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N, self.h = N, N.nvmlDeviceGetHandleByIndex(index)
+            self.fields = [(N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX, 0xFFFFFFFF),
+                           (N.NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_RX, 0xFFFFFFFF)]
+            if self.read() is None:
+                self.h = None
+        except Exception:
+            self.h = None
+
+    def read(self):
+        if self.h is None:
+            return None
+        try:
+            v = self.N.nvmlDeviceGetFieldValues(self.h, self.fields)
+        except Exception:
+            return None
+        if any(x.nvmlReturn != 0 for x in v):
+            return None
+        return tuple(int(x.value.ullVal) * 1024 for x in v)
+
+
+def busbw_suite(a, world, local, dev, opts, stream, flush_l2, barrier, max_over_ranks, reps=100):
+    """SURVEY §8(d) M-2 bucket busBW, per algorithm, on one 25 MiB bucket:
+    t = the WHOLE sync as the caller sees it — a CUDA event on the producer stream
+    before ddp_grad_ready and one after ddp_finalize_backward (which makes that
+    stream wait for every library stream) — median over `reps` reps, L2 flushed
+    between reps outside the events, max over ranks; busBW = (S/t) 2(W-1)/W.
+    'default' is the library's choice for this bucket as the LAST bucket of a pass
+    (fused kernels on all 148 SMs); 'nonlast' times the same bucket as bucket 0 of a
+    two-bucket pass (COMM_CTAS CTAs per lane) from the profile events around its
+    fused kernel.  'grad_view' runs the allreduce alone (gradient-as-bucket-view:
+    no pack / unpack).  NVLink TX / RX data bytes per rep from NVML counters."""
+    import statistics
+
+    import torch
+    from paper_2006_15704_b200 import _lib as L
+    from paper_2006_15704_b200.ddp import GradReducer
+    from synth import device as sdev
+
+    esize = 4 if a.dtype == "fp32" else 2
+    tdt = torch.float32 if a.dtype == "fp32" else torch.bfloat16
+    S = 25 * MIB
+    n25 = S // esize
+    nv = NvlinkCounter(local)
+    cfgs = [("default", {})] + [(L.ALGO_NAMES[x], {L.OPT_ALGO: x}) for x in
+                                (L.ALGO_ONESHOT, L.ALGO_TWOSHOT, L.ALGO_CE, L.ALGO_CE2, L.ALGO_PUSH, L.ALGO_NCCL,
+                                 L.ALGO_NVLS)]
+    cfgs.append(("grad_view", {L.OPT_GRAD_VIEW: 1}))
+    out = {"bucket_mib": 25, "reps": reps, "l2": "flushed between reps (outside the events)",
+           "timing": "producer-stream events around grad_ready -> finalize (whole sync), median, max over ranks",
+           "algorithmic_nvlink_bytes_per_direction": {
+               "oneshot/ce/push": (world - 1) * S, "twoshot/ce2/nccl(ring)": 2 * (world - 1) * S // world,
+               "nvls": S + S // world},
+           "per_algo": {}}
+    base = dict(opts)
+    base.pop(L.OPT_ALGO, None)
+    base.pop(L.OPT_GRAD_VIEW, None)
+    for name, extra in cfgs:
+        o = {**base, **extra}
+        red = GradReducer([n25], a.dtype, S, options=o)
+        algo = red.bucket_algos()[0]
+        if name == "nvls" and algo != "nvls":
+            red.close()
+            continue
+        if extra.get(L.OPT_GRAD_VIEW):
+            g = red._storage[L.ddp_param_storage_offset(red.ctx, 0):][:S].view(tdt)
+        else:
+            g = torch.empty(n25, dtype=tdt, device=dev)
+        sdev.fill(g, 15704, int(os.environ.get("RANK", 0)), 0, 0, "normal", a.dtype)
+
+        def one():
+            red.grad_ready(0, g, stream)
+            red.finalize(stream)
+        for _ in range(10):
+            one()
+        barrier()
+        c0 = nv.read()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for i in range(reps):
+            flush_l2()
+            evs[i][0].record(stream)
+            one()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+        c1 = nv.read()
+        ts = sorted(x.elapsed_time(y) for x, y in evs)
+        med = max_over_ranks(statistics.median(ts))
+        p10, p90 = max_over_ranks(ts[len(ts) // 10]), max_over_ranks(ts[(9 * len(ts)) // 10])
+        r = {"algo": algo, "ms": med, "ms_p10": p10, "ms_p90": p90,
+             "busbw_gbs": S / (med * 1e-3) * 2 * (world - 1) / world / 1e9,
+             "includes": "allreduce only (gradients are the bucket)" if extra.get(L.OPT_GRAD_VIEW)
+             else "pack x1/W + allreduce + unpack"}
+        if c0 is not None and c1 is not None:
+            # read after the warm-up reps; the L2 flushes are local HBM traffic only
+            r["nvlink_tx_bytes_per_rep"] = (c1[0] - c0[0]) / reps
+            r["nvlink_rx_bytes_per_rep"] = (c1[1] - c0[1]) / reps
+        red.close()
+        del g
+        if algo in ("oneshot", "twoshot", "nvls"):   # the same bucket as a NON-last bucket
+            red2 = GradReducer([1024, n25], a.dtype, S, options=o)
+            g2 = torch.empty(n25, dtype=tdt, device=dev)
+            gt = torch.empty(1024, dtype=tdt, device=dev)
+            sdev.fill(g2, 15704, 0, 0, 1, "normal", a.dtype)
+            sdev.fill(gt, 15704, 0, 0, 0, "normal", a.dtype)
+            L.ddp_set_option(red2.ctx, L.OPT_PROFILE, 1)
+
+            def two():
+                red2.grad_ready(1, g2, stream)
+                red2.grad_ready(0, gt, stream)
+                red2.finalize(stream)
+            for _ in range(5):
+                two()
+            L.ddp_profile_timeline(red2.ctx)
+            barrier()
+            for _ in range(reps // 2):
+                flush_l2()
+                two()
+            tl = L.ddp_profile_timeline(red2.ctx, cap=4 * reps)
+            first = [e_ - s_ for k, _, s_, e_ in tl[0::2] if k == "p2p_fused"]
+            if first:
+                t2 = max_over_ranks(statistics.median(first))
+                r["nonlast"] = {"ms": t2, "busbw_gbs": S / (t2 * 1e-3) * 2 * (world - 1) / world / 1e9,
+                                "ctas_per_rank": int(L.ddp_get_option(red2.ctx, L.OPT_COMM_CTAS)),
+                                "timing": "profile events around the fused kernel of bucket 0 (median)"}
+            red2.close()
+        out["per_algo"][name] = r
+    d = out["per_algo"].get("default")
+    if d:
+        out.update(value=d["busbw_gbs"], unit="GB/s", algo=d["algo"], ms=d["ms"],
+                   frac_of_nominal_900=d["busbw_gbs"] / 900.0, frac_of_measured_770=d["busbw_gbs"] / 770.0)
+    return out
 
 
 def build_model(name, dtype, batch, seq, rank, dev):
@@ -615,7 +742,7 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
             tot += s.elapsed_time(e)
         return tot
 
-    for _ in range(3):
+    for _ in range(10):
         one(True)
         one(False)
     if world > 1:
@@ -677,15 +804,29 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
     vals = [statistics.median(ts), statistics.median(tb), statistics.median(tn) if tn else 0.0]
     vals += [ns_res[n] for n in nosync_every] + [ns_base[n] for n in nosync_every]
     vals.append(statistics.median(fl))
+    # spread: paired differences of the interleaved (synced, no_sync) passes
+    dif = sorted(x - y for x, y in zip(ts, tb))
+
+    def pct(v, q):
+        return v[min(len(v) - 1, int(q * (len(v) - 1) + 0.5))]
+    spread = [pct(dif, 0.1), pct(dif, 0.5), pct(dif, 0.9), pct(sorted(tb), 0.1), pct(sorted(tb), 0.9)]
+    vals += spread
     vt = torch.tensor(vals, dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(vt, op=dist.ReduceOp.MAX)
     t_sync, t_bwd, t_noov = float(vt[0]), float(vt[1]), float(vt[2])
+    d10, d50, d90, b10, b90 = (float(x) for x in vt[-5:])
+    vt = vt[:-5]
     res = {"model": desc, "dtype": dtype, "bucket_cap_mib": cap_mib,
            "buckets": ddp.reducer.num_buckets, "bucket_algos": ddp.reducer.bucket_algos(),
            "t_bwd_ms": t_bwd, "t_bwd_plus_sync_ms": t_sync, "exposed_ms": t_sync - t_bwd,
            "exposed_pct_of_bwd": 100.0 * (t_sync - t_bwd) / t_bwd,
-           "iters": iters, "timing": "median of interleaved passes, max over ranks",
+           "iters": iters, "warmup": 10, "timing": "median of interleaved passes, max over ranks",
+           "exposed_paired_ms": {"p10": d10, "p50": d50, "p90": d90},
+           "exposed_paired_pct_of_bwd": {"p10": 100 * d10 / t_bwd, "p50": 100 * d50 / t_bwd, "p90": 100 * d90 / t_bwd},
+           "t_bwd_ms_p10_p90": [b10, b90],
+           "spread_doc": "percentiles of the per-pair difference (synced pass - the no_sync pass right after it), "
+                         "each percentile max over ranks",
            "floor_ms": float(vt[-1]),
            "floor_ok": bool(t_sync - t_bwd >= float(vt[-1]) * 0.9),
            "floor_doc": "whole sync of the last bucket alone (it cannot start before backward ends)",

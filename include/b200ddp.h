@@ -77,16 +77,17 @@ enum {
   DDP_OPT_PROFILE = 6,          /* 1: time every device launch with CUDA events */
   DDP_OPT_ALGO = 7,             /* force the bucket allreduce: 0 auto, 1 NCCL, 2 one-shot, 3 two-shot,
                                    4 copy-engine one-shot (world > 1), 5 NVLS (needs MULTICAST),
-                                   6 SM push + stream-ordered reduce, 7 copy-engine two-shot,
-                                   8 stream-ordered NVLS (world > 1) */
+                                   6 SM push + stream-ordered reduce, 7 copy-engine two-shot */
   DDP_OPT_PACK_CTAS = 8,        /* max CTAs of the HBM-bound kernels (pack, unpack, CE gather /
                                    reduce, world-1 fused kernel); 1..9472, default 4736 */
   DDP_OPT_P2P_STAGE_BYTES = 9,  /* 0 (default): one pipeline stage per CTA chunk; else split each
                                    CTA chunk into stages of this many bytes (one sync per stage) */
   DDP_OPT_FIND_UNUSED = 10,     /* 1: globally-unused-parameter detection:
                                    enables ddp_mark_unused, a participation bitmap and one extra
-                                   allreduce per synced pass; CREATED only (storage grows by one
-                                   bucket-region-sized scratch + the bitmap) */
+                                   allreduce per synced pass (the bitmaps travel by copy engine, one
+                                   transfer per peer ordered by stream memory operations, and are
+                                   summed on the comm stream); CREATED only (storage grows by one
+                                   bucket-region-sized scratch + 2W+1 bitmaps) */
   DDP_OPT_MULTICAST = 11,       /* 1: the caller will pass a multicast (NVLS) address of the storage
                                    to ddp_bind_device, enabling DDP_ALGO_NVLS; CREATED only.  Every
                                    rank must agree.  Never increases ddp_storage_bytes */
@@ -119,7 +120,7 @@ enum {
                                    the fastest kernel on every SM.  2 (SM kernels; chosen for bf16):
                                    at world 2 the one-shot kernel instead of the copy engines.
                                    Layout key */
-  DDP_OPT_GRAD_VIEW = 19        /* gradient-as-bucket-view (§8(f) N-3, zero-copy variant; the
+  DDP_OPT_GRAD_VIEW = 19,       /* gradient-as-bucket-view (§8(f) N-3, zero-copy variant; the
                                    paper's buckets hold copies, Alg. 1 L231-L232 / L246): 1 = the
                                    caller places each gradient AT its bucket slot in this rank's
                                    storage (ddp_param_storage_offset), so a3 and a6 vanish.  Every
@@ -133,10 +134,31 @@ enum {
                                    summation order).  A gradient passed at any other
                                    address is still correct: it is copied raw into its slot before
                                    and back after the allreduce.  Not combinable with FIND_UNUSED
-                                   or WIRE_BF16 (DDP_ERR_UNSUPPORTED).  Default 0; layout key */
+                                   or WIRE_BF16 (DDP_ERR_UNSUPPORTED).  At world > 2 every bucket
+                                   then uses CE2, including the last one (no fused two-shot on
+                                   every SM): measured slower than the default policy at W=4
+                                   (profiles/r01_grad_view.md).  Default 0; layout key */
+  DDP_OPT_P2P_TIMEOUT_MS = 20,  /* bound of every barrier spin inside the fused P2P / NVLS kernels
+                                   (%globaltimer); a peer that never arrives makes the waiting CTAs
+                                   give up, set the error word and exit -> DDP_ERR_TIMEOUT from
+                                   ddp_check_device_errors (poisons).  Default 30000; any time */
+  DDP_OPT_WAIT_TIMEOUT_MS = 21, /* peer emulation (b200ddp_emu.h) only: bound of a host wait for a
+                                   peer's step (default 60000); any time */
+  DDP_OPT_EMU_DEAD_RANK = 22    /* test support, cooperative emulation only (ddp_bind_emulated):
+                                   this rank's CTAs return at once and never signal, so the others
+                                   must time out (DDP_OPT_P2P_TIMEOUT_MS).  -1 (default) = none */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.
+ * Failure behaviour: the fused kernels (ONESHOT, TWOSHOT, NVLS) bound every wait
+ * for a peer (DDP_OPT_P2P_TIMEOUT_MS) and report DDP_ERR_TIMEOUT.  The copy-engine
+ * exchanges (CE, PUSH, CE2) and the find_unused bitmap exchange wait with
+ * cuStreamWaitValue32, which has no timeout: a peer that dies mid-pass leaves this
+ * rank's library streams (and every stream ordered after them) blocked, exactly
+ * as a dead peer leaves an NCCL collective blocked ("the backward pass
+ * could hang").  Recovery is process-level: destroy the context (the NCCL
+ * communicator is aborted when poisoned) and exit.
+ *
  *   NCCL:    pack kernel -> ncclAllReduce(sum) -> unpack kernel (DDP_OPT_GRAD_VIEW: in-place
  *            ncclAllReduce(avg) on the slots the gradients live in; no pack / unpack)
  *   ONESHOT: one fused sm_100a kernel: pack, push to every peer, rank-order reduce into .grad
@@ -153,12 +175,9 @@ enum {
  *            b's reduction on the second stream.
  *   CE2:     copy-engine two-shot: pack kernel -> reduce-scatter copies of shards -> rank-order
  *            shard reduce kernel -> all-gather copies -> unpack kernel, five streams ordered by
- *            stream memory operations; 2(W-1)/W S NVLink bytes per direction, no SM waits.
- *   NVLS2:   stream-ordered NVLS: pack kernel -> [stream memops] multimem.ld_reduce/st kernel on the
- *            own shard -> [stream memops] unpack kernel, three streams, no SM waits; (1+1/W) S
- *            NVLink bytes per direction.  Needs DDP_OPT_MULTICAST; otherwise resolves to CE2. */
+ *            stream memory operations; 2(W-1)/W S NVLink bytes per direction, no SM waits. */
 enum { DDP_ALGO_AUTO = 0, DDP_ALGO_NCCL = 1, DDP_ALGO_ONESHOT = 2, DDP_ALGO_TWOSHOT = 3, DDP_ALGO_CE = 4,
-       DDP_ALGO_NVLS = 5, DDP_ALGO_PUSH = 6, DDP_ALGO_CE2 = 7, DDP_ALGO_NVLS2 = 8 };
+       DDP_ALGO_NVLS = 5, DDP_ALGO_PUSH = 6, DDP_ALGO_CE2 = 7 };
 
 /* ---- construction (host only, deterministic, touches no GPU) -------------
  * Bucket assignment (Alg. 1 "allocate parameters to buckets in the

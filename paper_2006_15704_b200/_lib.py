@@ -25,10 +25,10 @@ FP32, BF16 = 0, 1
 OPT_OVERLAP, OPT_P2P_ONESHOT_MAX, OPT_P2P_TWOSHOT_MAX, OPT_COMM_CTAS, OPT_DRY_RUN, OPT_PROFILE, \
     OPT_ALGO, OPT_PACK_CTAS, OPT_P2P_STAGE_BYTES, OPT_FIND_UNUSED, OPT_MULTICAST, OPT_CE_STREAMS, \
     OPT_NCCL_COMMS, OPT_CE_DIRECT_BYTES, OPT_WIRE_BF16, OPT_LANES, OPT_LOW_PRIORITY, \
-    OPT_PREFER_OVERLAP, OPT_GRAD_VIEW = range(1, 20)
-ALGO_AUTO, ALGO_NCCL, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_CE, ALGO_NVLS, ALGO_PUSH, ALGO_CE2, ALGO_NVLS2 = range(9)
+    OPT_PREFER_OVERLAP, OPT_GRAD_VIEW, OPT_P2P_TIMEOUT_MS, OPT_WAIT_TIMEOUT_MS, OPT_EMU_DEAD_RANK = range(1, 23)
+ALGO_AUTO, ALGO_NCCL, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_CE, ALGO_NVLS, ALGO_PUSH, ALGO_CE2 = range(8)
 ALGO_NAMES = {ALGO_NCCL: "nccl", ALGO_ONESHOT: "oneshot", ALGO_TWOSHOT: "twoshot", ALGO_CE: "ce",
-              ALGO_NVLS: "nvls", ALGO_PUSH: "push", ALGO_CE2: "ce2", ALGO_NVLS2: "nvls2"}
+              ALGO_NVLS: "nvls", ALGO_PUSH: "push", ALGO_CE2: "ce2"}
 PROFILE_KINDS = ("pack", "nccl_allreduce", "unpack", "p2p_fused", "ce_copy", "ce_reduce")
 
 
@@ -59,6 +59,7 @@ _SIGS = {
     "ddp_get_nccl_id": (C.c_int, [C.c_char_p]),
     "ddp_bind_device": (C.c_int, [_P, C.c_int32, C.c_char_p, _P, C.POINTER(_P), _P]),
     "ddp_bind_emulated": (C.c_int, [_P, C.c_int32, _P, C.POINTER(_P), C.c_int64]),
+    "ddp_bind_peer_emulated": (C.c_int, [_P, C.c_int32, _P, C.POINTER(_P)]),
     "ddp_grad_ready": (C.c_int, [_P, C.c_int32, _P, _P]),
     "ddp_grads_ready": (C.c_int, [_P, C.c_int32, C.POINTER(C.c_int32), C.POINTER(_P), _P]),
     "ddp_finalize_backward": (C.c_int, [_P, _P]),
@@ -192,6 +193,11 @@ def ddp_bind_emulated(ctx: int, device: int, comm_stream: int, storages: Sequenc
                       grad_rank_stride_bytes: int) -> None:
     ptrs = (_P * len(storages))(*storages)
     _check(lib().ddp_bind_emulated(ctx, device, comm_stream, ptrs, grad_rank_stride_bytes))
+
+
+def ddp_bind_peer_emulated(ctx: int, device: int, comm_stream: int, storages: Sequence[int]) -> None:
+    ptrs = (_P * len(storages))(*storages)
+    _check(lib().ddp_bind_peer_emulated(ctx, device, comm_stream, ptrs))
 
 
 def ddp_grad_ready(ctx: int, param_idx: int, grad_ptr: int, producer_stream: int) -> None:

@@ -8,6 +8,7 @@
 #include <cuda.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <utility>
@@ -32,6 +33,9 @@ constexpr int64_t kMinChunkElems = 4096;   // smallest per-CTA chunk worth a CTA
 constexpr int64_t kBarrierScratch = 32 * 1024;  // scratch int inside the flags region
 constexpr int kMaxLanes = 4;
 constexpr int64_t kCeWireAlign = 64;  // elements: wire offsets keep 16-B (and 256-B) alignment
+constexpr int kCeFlagKinds = 4;       // stream-memop flags per bucket: ready, consumed, gathered, bitmap
+
+struct EmuGroup;  // peer emulation (core/emulation.cpp)
 
 struct Bucket {
   int64_t numel = 0;
@@ -93,9 +97,13 @@ struct ddp_ctx {
                              // (measured: exposed 3.1 -> 2.8% at W=2, 9.3 -> 9.0% at W=4)
   int64_t prefer_overlap = 0;  // policy for buckets synced under a running backward (see resolve_algo)
   int64_t grad_view = 0;       // N-3 zero-copy: gradients live in their bucket slots (NCCL in place)
+  int64_t p2p_timeout_ms = 30000;   // bound of every P2P / NVLS barrier spin (%globaltimer)
+  int64_t wait_timeout_ms = 60000;  // peer emulation: bound of a host wait for a peer's issue
+  int64_t emu_dead_rank = -1;       // test support (cooperative emulation): this rank never signals
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
-          stage1_stride = 0, ce_flags_off = 0, bitmap_off = 0, scratch_off = 0, storage_bytes = 0;
+          stage1_stride = 0, ce_flags_off = 0, bitmap_off = 0, bitmap_stride = 0, global_off = 0,
+          scratch_off = 0, storage_bytes = 0;
   // find_unused: local participation since the last
   // synced pass, this pass's locally-unused parameters and their destinations
   std::vector<uint8_t> used_local;
@@ -107,6 +115,7 @@ struct ddp_ctx {
   int32_t* global_host = nullptr;   // pinned: summed bitmap (D2H target)
   cudaEvent_t bitmap_done = nullptr;
   bool bitmap_valid = false;
+  uint32_t un_count = 0;            // synced find_unused passes (bitmap exchange flag value)
   // copy-engine path: reduce stream, events, driver stream-memory-op entry points
   cudaStream_t ce_red = nullptr, ce_pack = nullptr;
   cudaStream_t ce_ag = nullptr, ce_up = nullptr;  // CE2: all-gather copies, unpack
@@ -125,7 +134,14 @@ struct ddp_ctx {
   // protocol state
   State state = State::CREATED;
   bool bound = false, emulated = false, poisoned = false;
+  // peer emulation: this context is ONE of `world` contexts (one per rank) in one
+  // process on one device, each driven by its own host thread (core/emulation.cpp)
+  bool peer_emu = false;
+  EmuGroup* emu = nullptr;
+  cudaEvent_t emu_pre[kMaxLanes] = {};
   bool no_sync = false, pass_no_sync = false;
+  bool pass_launched = false;    // a device launch happened in the open pass
+  bool comm_done_valid = false;  // comm_done recorded by an earlier finalize
   std::vector<uint8_t> ready;
   std::vector<int32_t> pending;
   int32_t cursor = 0, n_ready = 0;
@@ -169,6 +185,13 @@ struct ddp_ctx {
 
 namespace b200ddp {
 
+// Lanes run spinning P2P kernels side by side: all of them must fit on the SMs at
+// once (one CTA per SM guaranteed), else a lane could wait for a peer lane that
+// cannot be scheduled.  Same options on every rank -> same choice everywhere.
+inline int lanes_in_use(const ddp_ctx* c) {
+  return c->lanes * std::min<int64_t>(c->comm_ctas, kMaxCtas) <= 148 ? (int)c->lanes : 1;
+}
+
 // error paths: record the message, poison the context (CUDA / NCCL failures are fatal)
 ddp_status_t cuda_fail(ddp_ctx* c, cudaError_t e, const char* what);
 ddp_status_t nccl_fail(ddp_ctx* c, ncclResult_t r, const char* what);
@@ -191,5 +214,22 @@ void prof_end(ddp_ctx* c, cudaStream_t s = nullptr);
 ddp_status_t device_range(ddp_ctx* c, int b0, int b1);
 // find_unused, end of a synced pass: bitmap allreduce + write-back (N-1)
 ddp_status_t finish_unused(ddp_ctx* c);
+// library side streams, events and stream-memop entry points (both bind paths)
+ddp_status_t create_side_streams(ddp_ctx* c);
+
+// ---- core/emulation.cpp (peer emulation: W contexts, one device, one host thread each) ----
+// join / leave the group of contexts sharing storages[0]; join blocks until every
+// rank has joined (the bind-time barrier of the multi-process path)
+ddp_status_t emu_join(ddp_ctx* c);
+void emu_leave(ddp_ctx* c);
+// a stream write of value v to addr has been issued (enqueued) by this host thread
+void emu_issued(ddp_ctx* c, const uint32_t* addr, uint32_t v);
+// block the host until some thread has issued a write of >= v to addr (bounded)
+ddp_status_t emu_await_issue(ddp_ctx* c, const uint32_t* addr, uint32_t v);
+// fused P2P kernels (they spin on peers' flags): the W ranks meet on the host and
+// ONE cooperative kernel runs all of them, ordered after / before each rank's lane stream
+ddp_status_t emu_p2p_launch(ddp_ctx* c, int algo, const SlotView& sv, const P2PLaunch& a, cudaStream_t ls,
+                            int lane);
+uint32_t emu_error_word(const ddp_ctx* c);
 
 }  // namespace b200ddp

@@ -34,19 +34,28 @@ void prof_end(ddp_ctx* c, cudaStream_t s) {
 
 typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 
-// ce flags of bucket b in a rank's storage: [0][b][src] ready, [1][b][src] consumed
+// ce flags of bucket b in a rank's storage: [0][b][src] ready, [1][b][src] consumed,
+// [2][b][src] gathered (CE2), [3][0][src] participation bitmap delivered (find_unused)
 uint32_t* ce_flag(const ddp_ctx* c, int r, int kind, int b, int src) {
   return reinterpret_cast<uint32_t*>(static_cast<char*>(c->storage[r]) + c->ce_flags_off) +
-         ((size_t)kind * c->buckets.size() + b) * kMaxWorld + src;
+         ((size_t)kind * c->buckets.size() + b) * kMaxWorld + src;  // kind < kCeFlagKinds
 }
 
 ddp_status_t ce_write(ddp_ctx* c, cudaStream_t s, uint32_t* addr, uint32_t v) {
   // default flags: a memory fence precedes the write (stream-scoped __threadfence_system)
   CUresult r = reinterpret_cast<StreamValueFn>(c->fn_write32)((CUstream)s, (CUdeviceptr)addr, v, 0);
   if (r != CUDA_SUCCESS) return cuda_fail(c, cudaErrorUnknown, "cuStreamWriteValue32");
+  if (c->peer_emu) emu_issued(c, addr, v);
   return DDP_OK;
 }
+// The wait is invisible to the CUDA scheduler.  Across processes each rank issues
+// its writes of a step before its waits of that step, so every wait's write is
+// enqueued somewhere; with every rank in ONE process (peer emulation) the host
+// additionally holds the wait back until the matching write has been issued, so
+// streams that share a hardware queue can never hold a wait ahead of its write.
 ddp_status_t ce_wait(ddp_ctx* c, cudaStream_t s, uint32_t* addr, uint32_t v) {
+  if (c->peer_emu)
+    if (ddp_status_t st = emu_await_issue(c, addr, v)) return st;
   CUresult r = reinterpret_cast<StreamValueFn>(c->fn_wait32)((CUstream)s, (CUdeviceptr)addr, v,
                                                               CU_STREAM_WAIT_VALUE_GEQ);
   if (r != CUDA_SUCCESS) return cuda_fail(c, cudaErrorUnknown, "cuStreamWaitValue32");
@@ -323,48 +332,6 @@ ddp_status_t launch_ce2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
   return DDP_OK;
 }
 
-// Stream-ordered NVLS (NVLS2): the three phases of the NVLS kernel as separate
-// kernels on three streams, ordered across ranks by stream memory operations,
-// so no kernel waits inside and consecutive buckets pipeline:
-//   pack stream:    pack x 1/W into the own bucket; "packed" flag to every peer
-//   reduce stream:  [wait all packed] own shard: multimem.ld_reduce + multimem.st
-//                   through the multicast address; "stored" flag to every peer
-//   unpack stream:  [wait all stored] own bucket -> .grad
-// Reuse: the next pass packs the bucket after this rank's unpack (finalize),
-// which followed every peer's "stored", which followed its ld_reduce reads.
-ddp_status_t launch_nvls2(ddp_ctx* c, int b, const SlotView& sv, float scale) {
-  Bucket& bk = c->buckets[b];
-  const int W = c->world, r = c->rank;
-  const uint32_t v = ++bk.ce_count;
-  char* own = static_cast<char*>(c->storage[r]) + bk.byte_off;
-  prof_begin(c, 0, c->ce_pack);
-  CUDA_TRY(c, launch_pack(c->dtype, sv, own, scale, (int)c->pack_ctas, c->ce_pack));
-  prof_end(c, c->ce_pack);
-  for (int i = 1; i < W; ++i)
-    if (ddp_status_t st = ce_write(c, c->ce_pack, ce_flag(c, (r + i) % W, 0, b, r), v)) return st;
-  CUDA_TRY(c, cudaEventRecord(c->ce_packed[b], c->ce_pack));
-  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_red, c->ce_packed[b], 0));
-  for (int i = 1; i < W; ++i)
-    if (ddp_status_t st = ce_wait(c, c->ce_red, ce_flag(c, r, 0, b, (r + i) % W), v)) return st;
-  const int64_t L = bk.shard;
-  const int64_t lo = std::min<int64_t>(r * L, bk.numel), hi = std::min<int64_t>(lo + L, bk.numel);
-  prof_begin(c, 3, c->ce_red);
-  CUDA_TRY(c, launch_nvls_reduce(c->dtype, static_cast<char*>(c->mc) + bk.byte_off, lo, hi, (int)c->pack_ctas,
-                                 c->ce_red));
-  prof_end(c, c->ce_red);
-  for (int i = 1; i < W; ++i)
-    if (ddp_status_t st = ce_write(c, c->ce_red, ce_flag(c, (r + i) % W, 2, b, r), v)) return st;
-  CUDA_TRY(c, cudaEventRecord(c->ce_reduced[b], c->ce_red));
-  CUDA_TRY(c, cudaStreamWaitEvent(c->ce_up, c->ce_reduced[b], 0));
-  for (int i = 1; i < W; ++i)
-    if (ddp_status_t st = ce_wait(c, c->ce_up, ce_flag(c, r, 2, b, (r + i) % W), v)) return st;
-  prof_begin(c, 2, c->ce_up);
-  CUDA_TRY(c, launch_unpack(c->dtype, sv, own, (int)c->pack_ctas, c->ce_up));
-  prof_end(c, c->ce_up);
-  c->ce2_used = true;  // joins ce_up at finalize
-  return DDP_OK;
-}
-
 // Gradient-as-bucket-view (N-3, zero-copy): the gradients normally ARE the
 // bucket's slots, so pack (Alg. 1) and the copy back (L246) vanish and
 // the bucket is averaged in place: ncclAvg multiplies every operand by fl(1/W)
@@ -390,7 +357,6 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   char* mine = static_cast<char*>(c->storage[c->rank]);
   if (bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH) return launch_ce(c, b);
   if (bk.algo == DDP_ALGO_CE2) return launch_ce2(c, b, sv, scale);
-  if (bk.algo == DDP_ALGO_NVLS2) return launch_nvls2(c, b, sv, scale);
   if (bk.algo == DDP_ALGO_NCCL) {
     void* buf = mine + bk.byte_off;
     const size_t k = c->rr_comm.empty() ? 0 : (size_t)b % c->rr_comm.size();
@@ -411,10 +377,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
     return DDP_OK;
   }
   // lane: its stream, flag table, sequence and staging (identical choice on every rank)
-  // Lanes run spinning kernels side by side: all of them must fit on the SMs at
-  // once (one CTA per SM guaranteed), else a lane could wait for a peer lane that
-  // cannot be scheduled.  Same options on every rank -> same choice everywhere.
-  const int nl = c->lanes * std::min<int64_t>(c->comm_ctas, kMaxCtas) <= 148 ? (int)c->lanes : 1;
+  const int nl = lanes_in_use(c);
   const int ln = (c->emulated || c->world == 1) ? 0 : b % nl;
   cudaStream_t ls = ln == 0 ? c->comm : c->lane_stream[ln];
   if (ln) c->lane_used[ln] = true;
@@ -470,11 +433,18 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   a.grad_rank_stride = c->grad_rank_stride;
   a.err = c->err_dev;
   a.mc = c->mc;
+  a.timeout_ns = (uint64_t)c->p2p_timeout_ms * 1000000ull;
+  a.dead_rank = (int32_t)c->emu_dead_rank;
   c->p2p_seq[ln] += (uint32_t)bk.stages + 2;  // flag values used: seq .. seq + stages + 1
   c->p2p_launches[ln] += 1;
   prof_begin(c, 3, ls);
-  if (bk.algo == DDP_ALGO_NVLS) CUDA_TRY(c, launch_nvls(c->dtype, sv, a, ls));
-  else CUDA_TRY(c, launch_p2p(bk.algo, c->dtype, sv, a, ls));
+  if (c->peer_emu) {  // the ranks meet on the host; one cooperative kernel runs them all
+    if (ddp_status_t st = emu_p2p_launch(c, bk.algo, sv, a, ls, ln)) return st;
+  } else if (bk.algo == DDP_ALGO_NVLS) {
+    CUDA_TRY(c, launch_nvls(c->dtype, sv, a, ls));
+  } else {
+    CUDA_TRY(c, launch_p2p(bk.algo, c->dtype, sv, a, ls));
+  }
   prof_end(c, ls);
   return DDP_OK;
 }
@@ -532,6 +502,21 @@ ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
     for (cudaStream_t q : c->ce2_rs) CUDA_TRY(c, cudaStreamWaitEvent(q, ev, 0));
   }
   c->unwaited.clear();
+  if (!c->pass_launched) {
+    // first launch of a pass: the library's side streams reuse staging / slots /
+    // flags the previous pass used, so order them after that pass's end even if
+    // the caller's producer stream is not ordered after its consumer stream
+    c->pass_launched = true;
+    if (c->comm_done_valid) {
+      for (cudaStream_t q : {c->ce_pack, c->ce_red, c->ce_up, c->ce_ag})
+        if (q) CUDA_TRY(c, cudaStreamWaitEvent(q, c->comm_done, 0));
+      for (cudaStream_t q : c->ce2_rs) CUDA_TRY(c, cudaStreamWaitEvent(q, c->comm_done, 0));
+      for (cudaStream_t q : c->ce2_ag) CUDA_TRY(c, cudaStreamWaitEvent(q, c->comm_done, 0));
+      for (int k = 1; k < kMaxLanes; ++k)
+        if (c->lane_stream[k]) CUDA_TRY(c, cudaStreamWaitEvent(c->lane_stream[k], c->comm_done, 0));
+      for (size_t k = 1; k < c->rr_stream.size(); ++k) CUDA_TRY(c, cudaStreamWaitEvent(c->rr_stream[k], c->comm_done, 0));
+    }
+  }
   if (c->world == 1 && !c->emulated) {
     // group maximal runs of world-1 fused buckets (slot table <= kMaxSlotsPerLaunch)
     int b = b0;
@@ -556,18 +541,40 @@ ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
   return DDP_OK;
 }
 
-// find_unused, end of a synced pass: local bitmap -> device (non-blocking
-// copy from pinned host memory), ONE extra allreduce (sum) of the bitmap on the
-// comm stream after every bucket, write-back of the locally-unused parameters
-// that some rank used, and the summed bitmap back to the host for
-// ddp_global_unused.  Then the local bitmap restarts (next synced window).
+// find_unused, end of a synced pass: the local participation bitmap
+// (pinned host -> own slot, non-blocking) is sent to slot r of every peer by the
+// copy engines (one transfer per peer, then a ready flag; double-buffered by pass
+// parity), the W slots are summed once every peer's flag has arrived (ONE extra
+// "allreduce" of the bitmap after every bucket, on the comm stream), the
+// locally-unused parameters that some rank used get their average, and the
+// summed bitmap goes back to the host for ddp_global_unused.  Then the local
+// bitmap restarts (next synced window).  Slot reuse: writing half v%2 again (pass
+// v+2) follows this rank's wait for the peer's pass-(v+1) flag, which the peer
+// wrote on its comm stream after its pass-v sum.
 ddp_status_t finish_unused(ddp_ctx* c) {
   const int32_t n = (int32_t)c->numel.size();
+  const int W = c->world, r = c->rank;
   if (c->bitmap_valid) CUDA_TRY(c, cudaEventSynchronize(c->bitmap_done));  // host buffers reusable
   for (int32_t p = 0; p < n; ++p) c->bitmap_host[p] = c->used_local[p];
-  int32_t* dev_bitmap = reinterpret_cast<int32_t*>(static_cast<char*>(c->storage[c->rank]) + c->bitmap_off);
-  CUDA_TRY(c, cudaMemcpyAsync(dev_bitmap, c->bitmap_host, (size_t)n * 4, cudaMemcpyHostToDevice, c->comm));
-  NCCL_TRY(c, ncclAllReduce(dev_bitmap, dev_bitmap, (size_t)n, ncclInt32, ncclSum, c->nccl, c->comm));
+  char* mine = static_cast<char*>(c->storage[r]);
+  int32_t* global = reinterpret_cast<int32_t*>(mine + c->global_off);
+  if (W == 1) {
+    CUDA_TRY(c, cudaMemcpyAsync(global, c->bitmap_host, (size_t)n * 4, cudaMemcpyHostToDevice, c->comm));
+  } else {
+    const uint32_t v = ++c->un_count;
+    const int64_t half = (int64_t)(v & 1) * W * c->bitmap_stride;
+    char* own = mine + c->bitmap_off + half + r * c->bitmap_stride;
+    CUDA_TRY(c, cudaMemcpyAsync(own, c->bitmap_host, (size_t)n * 4, cudaMemcpyHostToDevice, c->comm));
+    for (int i = 1; i < W; ++i) {
+      const int j = (r + i) % W;
+      char* dst = static_cast<char*>(c->storage[j]) + c->bitmap_off + half + r * c->bitmap_stride;
+      CUDA_TRY(c, cudaMemcpyAsync(dst, own, (size_t)n * 4, cudaMemcpyDeviceToDevice, c->comm));
+      if (ddp_status_t st = ce_write(c, c->comm, ce_flag(c, j, 3, 0, r), v)) return st;
+    }
+    for (int i = 1; i < W; ++i)
+      if (ddp_status_t st = ce_wait(c, c->comm, ce_flag(c, r, 3, 0, (r + i) % W), v)) return st;
+    CUDA_TRY(c, launch_bitmap_sum(W, mine + c->bitmap_off + half, c->bitmap_stride, global, n, c->comm));
+  }
   std::vector<const void*> src;
   std::vector<void*> dst;
   std::vector<int32_t> prm;
@@ -580,8 +587,8 @@ ddp_status_t finish_unused(ddp_ctx* c) {
     cnt.push_back(c->un_numel[k]);
   }
   const UnusedView uv{src.data(), dst.data(), prm.data(), cnt.data(), (int32_t)src.size()};
-  CUDA_TRY(c, launch_unused_fixup(c->dtype, uv, dev_bitmap, (int)c->pack_ctas, c->comm));
-  CUDA_TRY(c, cudaMemcpyAsync(c->global_host, dev_bitmap, (size_t)n * 4, cudaMemcpyDeviceToHost, c->comm));
+  CUDA_TRY(c, launch_unused_fixup(c->dtype, uv, global, (int)c->pack_ctas, c->comm));
+  CUDA_TRY(c, cudaMemcpyAsync(c->global_host, global, (size_t)n * 4, cudaMemcpyDeviceToHost, c->comm));
   CUDA_TRY(c, cudaEventRecord(c->bitmap_done, c->comm));
   c->bitmap_valid = true;
   std::fill(c->used_local.begin(), c->used_local.end(), 0);

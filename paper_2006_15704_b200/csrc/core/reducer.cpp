@@ -89,10 +89,8 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   int a;
   if (c->algo != DDP_ALGO_AUTO) {
     a = (int)c->algo;
-    if (c->world == 1 && (a == DDP_ALGO_CE || a == DDP_ALGO_NVLS || a == DDP_ALGO_PUSH || a == DDP_ALGO_CE2 ||
-                          a == DDP_ALGO_NVLS2))
+    if (c->world == 1 && (a == DDP_ALGO_CE || a == DDP_ALGO_NVLS || a == DDP_ALGO_PUSH || a == DDP_ALGO_CE2))
       a = DDP_ALGO_ONESHOT;
-    if (a == DDP_ALGO_NVLS2 && !c->multicast) a = DDP_ALGO_CE2;
     if (c->world > 1 && c->wire_bf16) a = DDP_ALGO_CE;  // the compressed wire is a CE feature
     if (a == DDP_ALGO_NVLS && !c->multicast) a = DDP_ALGO_TWOSHOT;
   } else if (c->world == 1) {
@@ -128,7 +126,7 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
 
 // Grid of a P2P launch: per-CTA chunks of >= kMinChunkElems, 256-element aligned.
 void grid_for(const ddp_ctx* c, Bucket& bk, int max_ctas) {
-  if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE2 || bk.algo == DDP_ALGO_NVLS2) {
+  if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE2) {
     bk.ctas = 0;
     bk.chunk = 0;
     if (bk.algo == DDP_ALGO_NCCL) bk.shard = 0;
@@ -152,9 +150,11 @@ void grid_for(const ddp_ctx* c, Bucket& bk, int max_ctas) {
 int max_ctas_for(const ddp_ctx* c, const Bucket& bk) {
   const bool last = &bk == &c->buckets.back() && c->world > 1;
   int m = c->world == 1 ? (int)c->pack_ctas : last ? std::min(148, kMaxCtas) : (int)std::min<int64_t>(c->comm_ctas, kMaxCtas);
-  if (c->emulated) {
+  if (c->emulated || c->peer_emu) {
+    // every rank of a launch in one cooperative kernel; in peer emulation the
+    // lanes' kernels must also fit side by side (they spin independently)
     const int e = emulated_max_ctas(bk.algo, c->dtype, (int)bk.params.size(), c->world);
-    m = std::min(m, std::max(1, e));
+    m = std::min(m, std::max(1, e / (c->peer_emu ? lanes_in_use(c) : 1)));
   }
   return std::max(1, m);
 }
@@ -179,15 +179,11 @@ void plan(ddp_ctx* c) {
   pos += c->lanes * 2 * c->world * c->stage1_stride;  // per lane, double-buffered by the lane's launch parity
   // copy-engine buckets: W slots each (dedicated per bucket) + ready/consumed flags
   c->ce_flags_off = pos;
-  pos += align_up((int64_t)c->buckets.size() * kMaxWorld * 3 * 4, 256);  // kinds: ready, consumed, gathered
+  pos += align_up((int64_t)c->buckets.size() * kMaxWorld * kCeFlagKinds * 4, 256);  // ready, consumed, gathered, bitmap
   for (Bucket& bk : c->buckets) {
     bk.ce_stride = 0;
     bk.ce_wire.clear();
     bk.ce_direct.clear();
-    if (bk.algo == DDP_ALGO_NVLS2) {  // no staging: the switch reads every rank's bucket
-      bk.shard = align_up(cdiv(bk.numel, c->world), kAlignElems);
-      continue;
-    }
     if (bk.algo == DDP_ALGO_CE2) {  // double-buffered reduce-scatter staging: [2][W] shard slots
       const int64_t L = align_up(cdiv(bk.numel, c->world), kAlignElems);
       bk.shard = L;
@@ -226,12 +222,17 @@ void plan(ddp_ctx* c) {
     bk.ce_off = pos;
     pos += c->world * bk.ce_stride;
   }
-  // find_unused: device bitmap (int32 per param) + a scratch copy of the bucket region
-  // (locally-unused parameters pack zeros from, and receive the average into, it)
-  c->bitmap_off = c->scratch_off = 0;
+  // find_unused: participation bitmaps (int32 per param; [2 pass parities][W source
+  // ranks] slots at world > 1, exchanged by the copy engines), the summed bitmap, and
+  // a scratch copy of the bucket region (locally-unused parameters pack zeros from,
+  // and receive the average into, it)
+  c->bitmap_off = c->global_off = c->scratch_off = c->bitmap_stride = 0;
   if (c->find_unused) {
+    c->bitmap_stride = align_up((int64_t)c->numel.size() * 4, 256);
     c->bitmap_off = pos;
-    pos += align_up((int64_t)c->numel.size() * 4, 256);
+    pos += (c->world > 1 ? 2 * c->world : 0) * c->bitmap_stride;
+    c->global_off = pos;
+    pos += c->bitmap_stride;
     c->scratch_off = pos;
     pos += c->stage2_off - c->buckets_off;  // = the bucket region
   }
@@ -266,6 +267,7 @@ ddp_status_t launch_range(ddp_ctx* c, int b0, int b1, int32_t trigger) {
 
 void open_pass(ddp_ctx* c) {
   c->state = State::IN_PASS;
+  c->pass_launched = false;
   c->pass_no_sync = c->no_sync;  // reading C-9
   std::fill(c->ready.begin(), c->ready.end(), 0);
   for (size_t b = 0; b < c->buckets.size(); ++b) c->pending[b] = (int32_t)c->buckets[b].params.size();
@@ -447,6 +449,9 @@ void ddp_destroy(ddp_ctx_t* c) {
   if (c->bitmap_host) cudaFreeHost(c->bitmap_host);
   if (c->global_host) cudaFreeHost(c->global_host);
   if (c->bitmap_done) cudaEventDestroy(c->bitmap_done);
+  for (cudaEvent_t e : c->emu_pre)
+    if (e) cudaEventDestroy(e);
+  emu_leave(c);
   delete c;
 }
 
@@ -520,6 +525,70 @@ static ddp_status_t bind_common(ddp_ctx* c, int32_t device, void* comm_stream) {
   return DDP_OK;
 }
 
+}  // extern "C"
+
+namespace b200ddp {
+
+// Zeroes this rank's barrier / stream-memop flags (on the comm stream) and creates
+// the library's side streams: lanes for the fused P2P kernels, the copy-engine
+// streams and events, and the stream-memory-operation entry points (world > 1).
+ddp_status_t create_side_streams(ddp_ctx* c) {
+  char* mine = static_cast<char*>(c->storage[c->rank]);
+  CUDA_TRY(c, cudaMemsetAsync(mine + c->flags_off, 0, c->lanes * kFlagsBytes, c->comm));
+  CUDA_TRY(c, cudaMemsetAsync(mine + c->ce_flags_off, 0, (size_t)c->buckets.size() * kMaxWorld * kCeFlagKinds * 4,
+                              c->comm));
+  int lo = 0, hi = 0;
+  CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  if (c->low_priority) hi = lo;  // side streams at the lowest priority
+  if (c->world > 1 && c->lanes > 1) {
+    for (int k = 1; k < c->lanes; ++k) {
+      CUDA_TRY(c, cudaStreamCreateWithPriority(&c->lane_stream[k], cudaStreamNonBlocking, hi));
+      CUDA_TRY(c, cudaEventCreateWithFlags(&c->lane_done[k], cudaEventDisableTiming));
+    }
+    for (int k = 0; k < c->lanes; ++k) CUDA_TRY(c, cudaEventCreateWithFlags(&c->lane_tail[k], cudaEventDisableTiming));
+  }
+  bool any_ce = false;
+  for (const Bucket& bk : c->buckets)
+    any_ce |= bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH || bk.algo == DDP_ALGO_CE2;
+  if (any_ce) {
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_red, cudaStreamNonBlocking, hi));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_pack, cudaStreamNonBlocking, hi));
+    c->ce_packed.assign(c->buckets.size(), nullptr);
+    for (auto& e : c->ce_packed) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ce_copied.assign(c->buckets.size(), nullptr);
+    for (auto& e : c->ce_copied) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_ag, cudaStreamNonBlocking, hi));
+    // CE2 copy streams: CE_STREAMS of them (peers round-robin).  One per peer was
+    // measured slower at W=4 (profiles/r01_n4.md): the copy engines do not overlap
+    // transfers usefully, the extra streams only add ordering hops
+    const size_t nst = (size_t)std::max<int64_t>(1, std::min<int64_t>(c->ce_streams, c->world - 1));
+    c->ce2_rs.assign(nst, nullptr);
+    c->ce2_ag.assign(nst, nullptr);
+    for (auto& q : c->ce2_rs) CUDA_TRY(c, cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
+    for (auto& q : c->ce2_ag) CUDA_TRY(c, cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
+    c->ce2_done.assign(2 * nst, nullptr);
+    for (auto& e : c->ce2_done) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_up, cudaStreamNonBlocking, hi));
+    c->tail_ev.assign(4, nullptr);
+    for (auto& e : c->tail_ev) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    c->ce_reduced.assign(c->buckets.size(), nullptr);
+    for (auto& e : c->ce_reduced) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ce_red_done, cudaEventDisableTiming));
+  }
+  if (c->world > 1) {  // copy-engine exchanges and the find_unused bitmap exchange
+    cudaDriverEntryPointQueryResult q1, q2;
+    CUDA_TRY(c, cudaGetDriverEntryPoint("cuStreamWriteValue32", &c->fn_write32, cudaEnableDefault, &q1));
+    CUDA_TRY(c, cudaGetDriverEntryPoint("cuStreamWaitValue32", &c->fn_wait32, cudaEnableDefault, &q2));
+    if (q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !c->fn_write32 || !c->fn_wait32)
+      return fail(DDP_ERR_UNSUPPORTED, "stream memory operations unavailable (copy-engine exchange)");
+  }
+  return DDP_OK;
+}
+
+}  // namespace b200ddp
+
+extern "C" {
+
 ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id[128], void* comm_stream,
                              void* const* peer_storage, void* multicast_ptr) {
   if (ddp_status_t st = check_ctx(c)) return st;
@@ -554,57 +623,8 @@ ddp_status_t ddp_bind_device(ddp_ctx_t* c, int32_t device, const uint8_t nccl_id
       CUDA_TRY(c, cudaEventCreateWithFlags(&c->rr_done[k], cudaEventDisableTiming));
     }
   }
+  if (ddp_status_t st = create_side_streams(c)) return st;
   char* mine = static_cast<char*>(c->storage[c->rank]);
-  CUDA_TRY(c, cudaMemsetAsync(mine + c->flags_off, 0, c->lanes * kFlagsBytes, c->comm));
-  if (c->world > 1 && c->lanes > 1) {
-    int lo = 0, hi = 0;
-    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    if (c->low_priority) hi = lo;  // side streams at the lowest priority
-    for (int k = 1; k < c->lanes; ++k) {
-      CUDA_TRY(c, cudaStreamCreateWithPriority(&c->lane_stream[k], cudaStreamNonBlocking, hi));
-      CUDA_TRY(c, cudaEventCreateWithFlags(&c->lane_done[k], cudaEventDisableTiming));
-    }
-    for (int k = 0; k < c->lanes; ++k) CUDA_TRY(c, cudaEventCreateWithFlags(&c->lane_tail[k], cudaEventDisableTiming));
-  }
-  CUDA_TRY(c, cudaMemsetAsync(mine + c->ce_flags_off, 0, (size_t)c->buckets.size() * kMaxWorld * 3 * 4, c->comm));
-  bool any_ce = false;
-  for (const Bucket& bk : c->buckets)
-    any_ce |= bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH || bk.algo == DDP_ALGO_CE2 ||
-              bk.algo == DDP_ALGO_NVLS2;
-  if (any_ce) {
-    int lo = 0, hi = 0;
-    CUDA_TRY(c, cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    if (c->low_priority) hi = lo;  // side streams at the lowest priority
-    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_red, cudaStreamNonBlocking, hi));
-    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_pack, cudaStreamNonBlocking, hi));
-    c->ce_packed.assign(c->buckets.size(), nullptr);
-    for (auto& e : c->ce_packed) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    c->ce_copied.assign(c->buckets.size(), nullptr);
-    for (auto& e : c->ce_copied) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_ag, cudaStreamNonBlocking, hi));
-    // CE2 copy streams: CE_STREAMS of them (peers round-robin).  One per peer was
-    // measured slower at W=4 (profiles/r01_n4.md): the copy engines do not overlap
-    // transfers usefully, the extra streams only add ordering hops
-    const size_t nst = (size_t)std::max<int64_t>(1, std::min<int64_t>(c->ce_streams, c->world - 1));
-    c->ce2_rs.assign(nst, nullptr);
-    c->ce2_ag.assign(nst, nullptr);
-    for (auto& q : c->ce2_rs) CUDA_TRY(c, cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
-    for (auto& q : c->ce2_ag) CUDA_TRY(c, cudaStreamCreateWithPriority(&q, cudaStreamNonBlocking, hi));
-    c->ce2_done.assign(2 * nst, nullptr);
-    for (auto& e : c->ce2_done) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_up, cudaStreamNonBlocking, hi));
-    c->tail_ev.assign(4, nullptr);
-    for (auto& e : c->tail_ev) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    c->ce_reduced.assign(c->buckets.size(), nullptr);
-    for (auto& e : c->ce_reduced) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-
-    CUDA_TRY(c, cudaEventCreateWithFlags(&c->ce_red_done, cudaEventDisableTiming));
-    cudaDriverEntryPointQueryResult q1, q2;
-    CUDA_TRY(c, cudaGetDriverEntryPoint("cuStreamWriteValue32", &c->fn_write32, cudaEnableDefault, &q1));
-    CUDA_TRY(c, cudaGetDriverEntryPoint("cuStreamWaitValue32", &c->fn_wait32, cudaEnableDefault, &q2));
-    if (q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !c->fn_write32 || !c->fn_wait32)
-      return fail(DDP_ERR_UNSUPPORTED, "stream memory operations unavailable (copy-engine algorithm)");
-  }
   // every rank's flags are zero before anyone's first P2P launch
   NCCL_TRY(c, ncclAllReduce(mine + kBarrierScratch, mine + kBarrierScratch, 1, ncclInt32, ncclSum, c->nccl, c->comm));
   CUDA_TRY(c, cudaStreamSynchronize(c->comm));
@@ -625,9 +645,9 @@ ddp_status_t ddp_bind_emulated(ddp_ctx_t* c, int32_t device, void* comm_stream, 
       return fail(DDP_ERR_INVALID_ARG, "storages must be non-null and 256-B aligned");
   }
   for (const Bucket& bk : c->buckets)
-    if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH || bk.algo == DDP_ALGO_CE2 ||
-        bk.algo == DDP_ALGO_NVLS2)
-      return fail(DDP_ERR_UNSUPPORTED, "emulation runs the one-shot / two-shot kernels only (set DDP_OPT_ALGO)");
+    if (bk.algo == DDP_ALGO_NCCL || bk.algo == DDP_ALGO_CE || bk.algo == DDP_ALGO_PUSH || bk.algo == DDP_ALGO_CE2)
+      return fail(DDP_ERR_UNSUPPORTED, "cooperative emulation runs the one-shot / two-shot kernels only (set "
+                                       "DDP_OPT_ALGO, or use ddp_bind_peer_emulated)");
   if (c->find_unused) return fail(DDP_ERR_UNSUPPORTED, "find_unused needs a real communicator (no emulation)");
   if (c->multicast) return fail(DDP_ERR_UNSUPPORTED, "NVLS needs real multicast memory (no emulation)");
   if (ddp_status_t st = bind_common(c, device, comm_stream)) return st;
@@ -638,6 +658,34 @@ ddp_status_t ddp_bind_emulated(ddp_ctx_t* c, int32_t device, void* comm_stream, 
   for (int r = 0; r < c->world; ++r)
     CUDA_TRY(c, cudaMemsetAsync(static_cast<char*>(c->storage[r]) + c->flags_off, 0, c->lanes * kFlagsBytes, c->comm));
   CUDA_TRY(c, cudaStreamSynchronize(c->comm));
+  c->bound = true;
+  c->state = State::IDLE;
+  return DDP_OK;
+}
+
+ddp_status_t ddp_bind_peer_emulated(ddp_ctx_t* c, int32_t device, void* comm_stream, void* const* storages) {
+  if (ddp_status_t st = check_ctx(c)) return st;
+  if (c->bound || c->state != State::CREATED) return fail(DDP_ERR_STATE, "already bound");
+  if (c->dry_run) return fail(DDP_ERR_STATE, "dry-run context cannot be bound");
+  if (c->world < 2) return fail(DDP_ERR_INVALID_ARG, "peer emulation needs world >= 2");
+  if (!storages) return fail(DDP_ERR_INVALID_ARG, "null storages");
+  for (int r = 0; r < c->world; ++r)
+    if (!storages[r] || (reinterpret_cast<uintptr_t>(storages[r]) & 255))
+      return fail(DDP_ERR_INVALID_ARG, "storages must be non-null and 256-B aligned");
+  if (c->multicast) return fail(DDP_ERR_UNSUPPORTED, "NVLS needs real multicast memory (no emulation)");
+  for (size_t b = 0; b < c->buckets.size(); ++b)
+    if (c->buckets[b].algo == DDP_ALGO_NCCL)
+      return fail(DDP_ERR_UNSUPPORTED, "peer emulation has no NCCL communicator: bucket " + std::to_string(b) +
+                                           " resolves to NCCL (> 1024 slots, TWOSHOT_MAX or DDP_OPT_ALGO)");
+  if (ddp_status_t st = bind_common(c, device, comm_stream)) return st;
+  for (int r = 0; r < c->world; ++r) c->storage[r] = storages[r];
+  c->peer_emu = true;
+  regrid(c);
+  if (ddp_status_t st = create_side_streams(c)) return st;
+  for (int k = 0; k < c->lanes; ++k) CUDA_TRY(c, cudaEventCreateWithFlags(&c->emu_pre[k], cudaEventDisableTiming));
+  CUDA_TRY(c, cudaStreamSynchronize(c->comm));
+  // every rank's flags are zero before any rank issues work (host barrier)
+  if (ddp_status_t st = emu_join(c)) return st;
   c->bound = true;
   c->state = State::IDLE;
   return DDP_OK;
@@ -742,6 +790,7 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
     }
     if (!c->dry_run) {
       CUDA_TRY(c, cudaEventRecord(c->comm_done, c->comm));
+      c->comm_done_valid = true;
       CUDA_TRY(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), c->comm_done, 0));
     }
   }
@@ -789,7 +838,7 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       c->twoshot_max = v;
       break;
     case DDP_OPT_ALGO:
-      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_NVLS2) return fail(DDP_ERR_INVALID_ARG, "bad algo");
+      if (v < DDP_ALGO_AUTO || v > DDP_ALGO_CE2) return fail(DDP_ERR_INVALID_ARG, "bad algo");
       c->algo = v;
       break;
     case DDP_OPT_FIND_UNUSED:
@@ -845,6 +894,18 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       c->pack_ctas = v;
       regrid(c);
       return DDP_OK;
+    case DDP_OPT_P2P_TIMEOUT_MS:
+      if (v < 1) return fail(DDP_ERR_INVALID_ARG, "P2P_TIMEOUT_MS must be >= 1");
+      c->p2p_timeout_ms = v;
+      return DDP_OK;
+    case DDP_OPT_WAIT_TIMEOUT_MS:
+      if (v < 1) return fail(DDP_ERR_INVALID_ARG, "WAIT_TIMEOUT_MS must be >= 1");
+      c->wait_timeout_ms = v;
+      return DDP_OK;
+    case DDP_OPT_EMU_DEAD_RANK:
+      if (v < -1 || v >= c->world) return fail(DDP_ERR_INVALID_ARG, "EMU_DEAD_RANK must be -1 or a rank");
+      c->emu_dead_rank = v;
+      return DDP_OK;
     case DDP_OPT_P2P_STAGE_BYTES:
       if (v < 0) return fail(DDP_ERR_INVALID_ARG, "negative stage bytes");
       c->stage_bytes = v;
@@ -879,6 +940,9 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_LOW_PRIORITY: *v = c->low_priority; break;
     case DDP_OPT_PREFER_OVERLAP: *v = c->prefer_overlap; break;
     case DDP_OPT_GRAD_VIEW: *v = c->grad_view; break;
+    case DDP_OPT_P2P_TIMEOUT_MS: *v = c->p2p_timeout_ms; break;
+    case DDP_OPT_WAIT_TIMEOUT_MS: *v = c->wait_timeout_ms; break;
+    case DDP_OPT_EMU_DEAD_RANK: *v = c->emu_dead_rank; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;
@@ -974,7 +1038,7 @@ ddp_status_t ddp_profile_timeline(ddp_ctx_t* c, int32_t cap, int32_t* kinds, dou
 
 ddp_status_t ddp_check_device_errors(ddp_ctx_t* c) {
   if (ddp_status_t st = check_ctx(c)) return st;
-  if (c->err_host && *reinterpret_cast<volatile uint32_t*>(c->err_host)) {
+  if ((c->err_host && *reinterpret_cast<volatile uint32_t*>(c->err_host)) || emu_error_word(c)) {
     c->poisoned = true;
     return fail(DDP_ERR_TIMEOUT, "a peer never reached a P2P barrier (timeout)");
   }

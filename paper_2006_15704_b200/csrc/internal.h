@@ -43,6 +43,8 @@ struct P2PLaunch {
   int64_t grad_rank_stride;   // emulation: byte distance between ranks' gradients
   uint32_t* err;              // device-visible error word (mapped pinned host memory)
   void* mc;                   // NVLS: multicast address of the storage base (NULL otherwise)
+  uint64_t timeout_ns;        // bound of every barrier spin (%globaltimer), then *err = 1
+  int32_t dead_rank;          // test support (emulation): this rank returns at once, never signals
 };
 
 // Several buckets launched together at world 1: slot k covers virtual elements
@@ -64,8 +66,6 @@ cudaError_t launch_unpack(int dtype, const SlotView& sv, const void* bucket, int
 cudaError_t launch_p2p(int algo, int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
 // NVLS (NVSwitch multicast) two-shot: pack -> multimem.ld_reduce + multimem.st -> unpack.
 cudaError_t launch_nvls(int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
-// NVLS2 reduce phase: bucket elements [lo, hi) through its multicast address.
-cudaError_t launch_nvls_reduce(int dtype, void* mc_bucket, int64_t lo, int64_t hi, int max_ctas, cudaStream_t s);
 // Copy-engine algorithm, SM part.  A list of gradients with their element
 // offsets inside a slot ("wire layout").
 struct CeView {
@@ -92,6 +92,10 @@ cudaError_t launch_wire_reduce(int world, int rank, const CeView& v, const void*
 // v_q = slot q (slot0 + q * stride_bytes) at wire_k + i.
 cudaError_t launch_ce_reduce(int dtype, int world, int rank, const CeView& v, const void* slot0,
                              int64_t stride_bytes, float scale, int max_ctas, cudaStream_t s);
+// find_unused bitmap exchange: global[p] = sum_{q<world} slot_q[p] (int32), slot_q =
+// slot0 + q * stride_bytes (each rank's local participation bitmap).
+cudaError_t launch_bitmap_sum(int world, const void* slot0, int64_t stride_bytes, int32_t* global, int32_t n,
+                              cudaStream_t s);
 // Locally-unused parameters (find_unused): copy src (library scratch holding the
 // average) -> dst (the caller's gradient) where global_used[param] > 0.
 struct UnusedView {

@@ -11,8 +11,6 @@ namespace b200ddp {
 
 namespace {
 
-constexpr uint64_t kTimeoutNs = 30ull * 1000 * 1000 * 1000;
-
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -54,7 +52,7 @@ __device__ __forceinline__ void p2p_wait(const P2PLaunch& a, int r, int kind, ui
       uint32_t v;
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
       if ((int32_t)(v - val) >= 0) break;
-      if (globaltimer() - t0 > kTimeoutNs) {
+      if (globaltimer() - t0 > a.timeout_ns) {
         atomicExch(a.err, 1u);
         break;
       }

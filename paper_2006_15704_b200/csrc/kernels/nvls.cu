@@ -151,36 +151,7 @@ cudaError_t dispatch(const SlotView& sv, const P2PLaunch& a, cudaStream_t st) {
   return cudaErrorInvalidValue;
 }
 
-// NVLS2 reduce phase alone: elements [lo, hi) of the bucket at multicast address
-// mcb (hi rounded up to a whole 16-B vector; the bucket region is padded).
-template <typename T>
-__global__ void __launch_bounds__(kThreads) nvls_reduce_kernel(char* mcb, int64_t v0, int64_t nv) {
-  constexpr int U = 8;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  for (; v + (U - 1) * stride < nv; v += U * stride) {
-    uint4 x[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) x[u] = Mm<T>::ld_reduce(mcb + (v0 + v + u * stride) * 16);
-#pragma unroll
-    for (int u = 0; u < U; ++u) Mm<T>::st(mcb + (v0 + v + u * stride) * 16, x[u]);
-  }
-  for (; v < nv; v += stride) Mm<T>::st(mcb + (v0 + v) * 16, Mm<T>::ld_reduce(mcb + (v0 + v) * 16));
-}
-
 }  // namespace
-
-cudaError_t launch_nvls_reduce(int dtype, void* mc_bucket, int64_t lo, int64_t hi, int max_ctas, cudaStream_t s) {
-  if (hi <= lo || !mc_bucket) return cudaSuccess;
-  const int64_t ve = dtype == 0 ? 4 : 8;
-  const int64_t v0 = lo / ve, nv = (hi + ve - 1) / ve - v0;
-  int64_t grid = (nv + kThreads * 8 - 1) / (kThreads * 8);
-  if (grid > max_ctas) grid = max_ctas;
-  if (grid < 1) grid = 1;
-  if (dtype == 0) nvls_reduce_kernel<float><<<(int)grid, kThreads, 0, s>>>(static_cast<char*>(mc_bucket), v0, nv);
-  else nvls_reduce_kernel<__nv_bfloat16><<<(int)grid, kThreads, 0, s>>>(static_cast<char*>(mc_bucket), v0, nv);
-  return cudaGetLastError();
-}
 
 cudaError_t launch_nvls(int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s) {
   return dtype == 0 ? dispatch<float>(sv, a, s) : dispatch<__nv_bfloat16>(sv, a, s);

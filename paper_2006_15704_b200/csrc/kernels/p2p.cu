@@ -45,6 +45,7 @@ template <typename T, int W, int MAXS>
 __global__ void __launch_bounds__(kThreads, 1)
     twoshot_kernel(const __grid_constant__ SlotArgs<MAXS> sa, const __grid_constant__ P2PLaunch a) {
   const int r = a.emulated ? (int)blockIdx.y : a.rank;
+  if (a.emulated && r == a.dead_rank) return;  // test support: a peer that never arrives
   const int64_t gstride = a.emulated ? (int64_t)r * a.grad_rank_stride : 0;
   const int c = blockIdx.x;
   const int64_t L = a.shard, N = a.numel, Q = a.chunk, SUB = a.sub;
@@ -116,6 +117,7 @@ template <typename T, int W, int MAXS>
 __global__ void __launch_bounds__(kThreads, 1)
     oneshot_kernel(const __grid_constant__ SlotArgs<MAXS> sa, const __grid_constant__ P2PLaunch a) {
   const int r = a.emulated ? (int)blockIdx.y : a.rank;
+  if (a.emulated && r == a.dead_rank) return;  // test support: a peer that never arrives
   const int64_t gstride = a.emulated ? (int64_t)r * a.grad_rank_stride : 0;
   const int64_t lo0 = min((int64_t)blockIdx.x * a.chunk, a.numel);
   const int64_t hi0 = min(lo0 + a.chunk, a.numel);

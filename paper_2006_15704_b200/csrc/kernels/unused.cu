@@ -8,6 +8,9 @@
 //     (untouched)                otherwise ("DDP should only touch
 //                                 gradients that are indeed involved")
 // One launch for all such parameters; HBM-bound, 2 x bytes of the copied ones.
+// The participation bitmaps themselves travel as W slots per rank (copy-engine
+// transfers ordered by stream memory operations, core/exchange.cpp) and are
+// summed here in one small kernel (bitmap_sum_kernel).
 #include "common.cuh"
 
 namespace b200ddp {
@@ -81,7 +84,25 @@ cudaError_t dispatch(const UnusedView& uv, const int32_t* global_used, int max_c
   return cudaSuccess;
 }
 
+__global__ void __launch_bounds__(kThreads) bitmap_sum_kernel(const char* __restrict__ slot0, int64_t stride,
+                                                             int world, int32_t* __restrict__ global, int32_t n) {
+  for (int32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    int32_t s = 0;
+    for (int q = 0; q < world; ++q) s += __ldcg(reinterpret_cast<const int32_t*>(slot0 + q * stride) + p);
+    global[p] = s;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_bitmap_sum(int world, const void* slot0, int64_t stride_bytes, int32_t* global, int32_t n,
+                              cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  int grid = (n + kThreads - 1) / kThreads;
+  if (grid > 148) grid = 148;
+  bitmap_sum_kernel<<<grid, kThreads, 0, s>>>(static_cast<const char*>(slot0), stride_bytes, world, global, n);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_unused_fixup(int dtype, const UnusedView& uv, const int32_t* global_used, int max_ctas,
                                 cudaStream_t s) {
