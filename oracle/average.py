@@ -32,6 +32,8 @@ Two definitions are provided:
 
 from __future__ import annotations
 
+import math
+from fractions import Fraction
 from typing import List, Sequence, Tuple
 
 import numpy as np
@@ -86,17 +88,65 @@ def round_fp64_to(x: np.ndarray, dtype: str) -> np.ndarray:
 
 # ---- O-3 ----------------------------------------------------------------------
 
+def _round_fraction(x: Fraction, dtype: str) -> float:
+    """Exact RNE of a rational to the storage dtype's precision (fp32: 24
+    significant bits, bf16: 8), normal range; ties to the even significand."""
+    if x == 0:
+        return 0.0
+    bits = 24 if dtype == "fp32" else 8
+    _, e = math.frexp(float(abs(x)))
+    # pick e so that 2^(e-1) <= |x| < 2^e exactly (the float estimate may be off by one)
+    while Fraction(2) ** (e - 1) > abs(x):
+        e -= 1
+    while Fraction(2) ** e <= abs(x):
+        e += 1
+    q = Fraction(2) ** (e - bits)                 # spacing of the target grid in [2^(e-1), 2^e)
+    lo = (abs(x) / q).__floor__()
+    rem = abs(x) / q - lo
+    up = rem > Fraction(1, 2) or (rem == Fraction(1, 2) and lo % 2 == 1)
+    v = float((lo + (1 if up else 0)) * q)
+    return v if x > 0 else -v
+
+
 def average_fp64(grads: Sequence[np.ndarray], dtype: str) -> Tuple[np.ndarray, np.ndarray]:
     """grads[r] = rank r's gradient (same shape).  Returns (ref, den) where
-    ref is in the storage dtype and den is fp64."""
+    ref = RNE_dtype( (sum_r g_r) / W ) rounded ONCE from the exact rational
+    value, and den = (sum_r |g_r|) / W in fp64.
+
+    The sum runs in fp64 with an error-free transformation (TwoSum) per add, so
+    every element knows whether its fp64 sum is exact.  A value computed in fp64
+    rounds to the target like the exact value unless it sits exactly on a
+    target rounding midpoint (midpoints are fp64 numbers, and rounding is
+    monotonic); only elements that are on a midpoint AND whose fp64 sum or
+    quotient was inexact are recomputed with exact rationals."""
     W = len(grads)
     xs = [to_fp32(g, dtype).astype(np.float64) for g in grads]
     tot = np.zeros_like(xs[0])
     absum = np.zeros_like(xs[0])
+    inexact = np.zeros(tot.shape, dtype=bool)
     for x in xs:
-        tot += x          # exact enough: fp64 over <= 8 fp32 values (see DESIGN.md)
+        s = tot + x
+        bb = s - tot
+        err = (tot - (s - bb)) + (x - bb)      # TwoSum: tot + x == s + err exactly
+        inexact |= err != 0
+        tot = s
         absum += np.abs(x)
-    return round_fp64_to(tot / W, dtype), absum / W
+    q = tot / W
+    if W & (W - 1):                            # W not a power of two: the quotient may be rounded
+        inexact[...] = True
+    ref = round_fp64_to(q, dtype)
+    m, _ = np.frexp(q)
+    scaled = np.ldexp(m, 24 if dtype == "fp32" else 8)
+    midpoint = (scaled - np.floor(scaled)) == 0.5
+    redo = np.nonzero(np.ravel(midpoint & inexact))[0]
+    if redo.size:
+        flat_ref = ref.reshape(-1)
+        flat = [np.ravel(x) for x in xs]
+        for i in redo:
+            exact = sum((Fraction(float(x[i])) for x in flat), Fraction(0)) / W
+            v = np.array([_round_fraction(exact, dtype)], dtype=np.float64)
+            flat_ref[i] = round_fp64_to(v, dtype)[0]   # exact: v has <= 24 (8) significant bits
+    return ref, absum / W
 
 
 # ---- O-3b ---------------------------------------------------------------------

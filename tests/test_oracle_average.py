@@ -162,3 +162,28 @@ def test_round_fp64_to_bf16_single_rounding():
     got = to_fp32(round_fp64_to(v, "bf16"), "bf16")
     for a, b in zip(v, got):
         assert Fraction(float(b)) == _exact_rne(Fraction(float(a)), 8)
+
+
+def _f32(*vs):
+    return [np.array([v], dtype=np.float32) for v in vs]
+
+
+def test_o3_single_rounding_when_the_fp64_sum_is_inexact():
+    """O-3 rounds the EXACT average once.  Hand-derived closed forms where a
+    double rounding (fp64 sum, then the target) lands on a target midpoint and
+    ties the wrong way:
+      W=4: (2 + 2^-23 + 2^-80 + 0)/4 = 0.5 + 2^-25 + 2^-82 -> above the fp32
+           midpoint 0.5 + 2^-25 -> 0.5 + 2^-24  (fp64 drops 2^-80: tie -> 0.5);
+      W=3: (3 + 3*2^-24 + 2^-60)/3 = 1 + 2^-24 + 2^-60/3 -> 1 + 2^-23
+           (fp64: exactly the midpoint 1 + 2^-24 -> 1.0);
+      bf16, W=4: (2 + 2^-7 + 2^-80 + 0)/4 -> 0.5 + 2^-8 (bf16 spacing 2^-8)."""
+    ref, _ = average_fp64(_f32(2.0, 2.0 ** -23, 2.0 ** -80, 0.0), "fp32")
+    assert ref[0] == np.float32(0.5 + 2.0 ** -24)
+    ref, _ = average_fp64(_f32(3.0, 3 * 2.0 ** -24, 2.0 ** -60), "fp32")
+    assert ref[0] == np.float32(1 + 2.0 ** -23)
+    b = [round_fp32_to(x, "bf16") for x in _f32(2.0, 2.0 ** -7, 2.0 ** -80, 0.0)]
+    ref, _ = average_fp64(b, "bf16")
+    assert to_fp32(ref, "bf16")[0] == np.float32(0.5 + 2.0 ** -8)
+    # and a negative mirror image: the sign is carried through
+    ref, _ = average_fp64(_f32(-2.0, -(2.0 ** -23), -(2.0 ** -80), 0.0), "fp32")
+    assert ref[0] == np.float32(-(0.5 + 2.0 ** -24))

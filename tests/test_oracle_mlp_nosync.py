@@ -140,3 +140,15 @@ def test_empty_scope_is_normal_sync_and_scope_has_no_launches():
     order = [5, 4, 3, 2, 1, 0]
     assert replay(a, order, no_sync=True) == []
     assert [b for b, _ in replay(a, order)] == [0, 1, 2, 3]
+
+
+def test_accumulate_bf16_rounds_every_add():
+    """A bf16 ``.grad += g`` rounds after EVERY add (gradients are
+    accumulated into the same tensor).  1 + 2^-8 is the bf16 midpoint between 1
+    and 1 + 2^-7 and ties to the even 1, twice: sequential bf16 adds give 1.0,
+    while one rounding of the fp32 sum would give 1 + 2^-7."""
+    from oracle.average import round_fp32_to, to_fp32
+    micro = [round_fp32_to(np.array([v], dtype=np.float32), "bf16") for v in (1.0, 2.0 ** -8, 2.0 ** -8)]
+    assert to_fp32(accumulate(micro, "bf16"), "bf16")[0] == 1.0
+    micro = [round_fp32_to(np.array([v], dtype=np.float32), "bf16") for v in (2.0 ** -8, 2.0 ** -8, 1.0)]
+    assert to_fp32(accumulate(micro, "bf16"), "bf16")[0] == np.float32(1 + 2.0 ** -7)   # order matters
