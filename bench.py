@@ -61,6 +61,7 @@ def parse():
     ap.add_argument("--high-priority", action="store_true",
                     help="communication streams at the highest priority (default: lowest)")
     ap.add_argument("--lanes", type=int, default=0, help="P2P/NVLS kernel lanes (streams)")
+    ap.add_argument("--p2p-push", action="store_true", help="round-1 push kernels instead of the pull kernels")
     ap.add_argument("--wire-bf16", action="store_true", help="N-3: fp32 gradients travel as bf16 (CE exchange)")
     ap.add_argument("--grad-view", action="store_true",
                     help="N-3 zero-copy: gradients live in their bucket slots (in-place NCCL, no pack/unpack)")
@@ -239,6 +240,8 @@ def run_ours(a):
         opts[L.OPT_LOW_PRIORITY] = 0
     if a.lanes:
         opts[L.OPT_LANES] = a.lanes
+    if a.p2p_push:
+        opts[L.OPT_P2P_PULL] = 0
     if a.wire_bf16:
         opts[L.OPT_WIRE_BF16] = 1
     if a.grad_view:
@@ -755,7 +758,7 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
             ddp.reducer.set_option(L.OPT_OVERLAP, 0)   # paper's non-overlapped baseline
             tn.append(one(True))
             ddp.reducer.set_option(L.OPT_OVERLAP, 1)
-    ns_res, ns_base = {}, {}
+    ns_res, ns_base, ns_spread = {}, {}, {}
     for n in nosync_every:
         group(n)
         group(n, False)
@@ -764,6 +767,8 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
             gt.append(group(n))
             gb.append(group(n, False))
         ns_res[n], ns_base[n] = statistics.median(gt), statistics.median(gb)
+        dd = sorted(x - y for x, y in zip(gt, gb))
+        ns_spread[n] = (dd[len(dd) // 10], dd[(9 * len(dd)) // 10])
     # one profiled synced pass: Fig. 2(c)-style ready / start / end timeline of the comm launches
     ddp.reducer.set_option(L.OPT_PROFILE, 1)
     L.ddp_profile_timeline(ddp.reducer.ctx)
@@ -836,9 +841,14 @@ def exposed_for(model, fwd, desc, cap_mib, opts, iters, rank, world, local, dev,
         res["exposed_no_overlap_ms"] = t_noov - t_bwd
     if nosync_every:
         k = len(nosync_every)
+        sp = torch.tensor([x for n in nosync_every for x in ns_spread[n]], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(sp, op=dist.ReduceOp.MAX)
         res["nosync"] = {str(n): {"ms_per_iter": float(vt[3 + i]) / n,
                                   "no_sync_baseline_ms_per_iter": float(vt[3 + k + i]) / n,
-                                  "exposed_ms_per_iter": (float(vt[3 + i]) - float(vt[3 + k + i])) / n}
+                                  "exposed_ms_per_iter": (float(vt[3 + i]) - float(vt[3 + k + i])) / n,
+                                  "exposed_ms_per_iter_p10_p90": [float(sp[2 * i]) / n, float(sp[2 * i + 1]) / n],
+                                  "groups": max(2, iters // 2)}
                          for i, n in enumerate(nosync_every)}
         res["nosync_doc"] = ("group of n backward passes with .grad accumulation: n-1 inside no_sync + 1 synced "
                              "(ms_per_iter) vs all n inside no_sync (baseline); exposed = difference / n")
@@ -885,6 +895,8 @@ def _opts(a):
         o[L.OPT_LOW_PRIORITY] = 0
     if a.lanes:
         o[L.OPT_LANES] = a.lanes
+    if a.p2p_push:
+        o[L.OPT_P2P_PULL] = 0
     if a.wire_bf16:
         o[L.OPT_WIRE_BF16] = 1
     if a.grad_view:

@@ -144,9 +144,23 @@ enum {
                                    ddp_check_device_errors (poisons).  Default 30000; any time */
   DDP_OPT_WAIT_TIMEOUT_MS = 21, /* peer emulation (b200ddp_emu.h) only: bound of a host wait for a
                                    peer's step (default 60000); any time */
-  DDP_OPT_EMU_DEAD_RANK = 22    /* test support, cooperative emulation only (ddp_bind_emulated):
+  DDP_OPT_EMU_DEAD_RANK = 22,   /* test support, cooperative emulation only (ddp_bind_emulated):
                                    this rank's CTAs return at once and never signal, so the others
                                    must time out (DDP_OPT_P2P_TIMEOUT_MS).  -1 (default) = none */
+  DDP_OPT_P2P_PULL = 23,        /* fused ONESHOT / TWOSHOT kernels at world > 1: 1 (default) pull
+                                   form — each rank packs into its own bucket buffer (two per bucket,
+                                   alternating by pass) and reads its peers' buffers; the release
+                                   before each flag drains local stores only, .grad is written by
+                                   the reads (no unpack pass, no closing barrier).  0: push form
+                                   (remote stores into per-lane staging, round 1).  Layout key */
+  DDP_OPT_P2P_SIGNAL = 24,      /* pull kernels, measurement knob: how "my stores are done" is
+                                   published.  0 (default): bar.sync, fence.sc.sys, st.release.sys of
+                                   the flag into each peer; 1: bar.sync, st.release.sys only; 2:
+                                   bar.sync, fence.acq_rel.gpu, st.relaxed.sys into each peer; 3:
+                                   bar.sync, st.release.gpu of a flag in the OWN storage, which the
+                                   peers poll over NVLink (ld.acquire.sys).  Any time */
+  DDP_OPT_P2P_DEBUG = 25        /* measurement only (wrong results!): 1 skips the pull kernels'
+                                   data reads (syncs kept), 2 skips their pack.  Default 0 */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.

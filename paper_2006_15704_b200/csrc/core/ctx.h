@@ -43,6 +43,8 @@ struct Bucket {
   std::vector<int64_t> off;     // slot offsets, n+1 entries
   std::vector<void*> grads;     // slot -> gradient pointer supplied this pass
   int64_t byte_off = 0;         // inside the symmetric storage
+  int64_t alt_off = 0;          // pull kernels: second buffer (pass parity), inside the storage
+  uint32_t p2p_count = 0;       // fused launches of this bucket so far (pass parity)
   int algo = DDP_ALGO_NCCL;
   int ctas = 1;
   int64_t shard = 0, chunk = 0, sub = 0;
@@ -100,6 +102,9 @@ struct ddp_ctx {
   int64_t p2p_timeout_ms = 30000;   // bound of every P2P / NVLS barrier spin (%globaltimer)
   int64_t wait_timeout_ms = 60000;  // peer emulation: bound of a host wait for a peer's issue
   int64_t emu_dead_rank = -1;       // test support (cooperative emulation): this rank never signals
+  int64_t p2p_pull = 1;             // fused P2P kernels: 1 pull (kernels/pull.cu), 0 push (kernels/p2p.cu)
+  int64_t p2p_signal = 0;           // pull kernels: flag publication mode (DDP_OPT_P2P_SIGNAL)
+  int64_t p2p_debug = 0;            // measurement only: skip data phases (DDP_OPT_P2P_DEBUG)
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
           stage1_stride = 0, ce_flags_off = 0, bitmap_off = 0, bitmap_stride = 0, global_off = 0,

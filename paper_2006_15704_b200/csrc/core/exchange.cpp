@@ -409,7 +409,12 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   for (int r = 0; r < c->world; ++r) a.storage[r] = c->storage[r];
   a.flags_byte_off = c->flags_off + ln * kFlagsBytes;
   a.bucket_byte_off = bk.byte_off;
-  if (bk.algo == DDP_ALGO_TWOSHOT) {
+  a.pull = c->p2p_pull && c->world > 1 && bk.algo != DDP_ALGO_NVLS ? 1 : 0;
+  if (a.pull) {  // this pass's buffer of the bucket (pass parity, identical on every rank)
+    a.bucket_byte_off = (bk.p2p_count++ & 1) ? bk.alt_off : bk.byte_off;
+    a.stage_byte_off = 0;
+    a.stage_stride = 0;
+  } else if (bk.algo == DDP_ALGO_TWOSHOT) {
     a.stage_byte_off = c->stage2_off + ln * c->world * c->stage2_stride;
     a.stage_stride = c->stage2_stride;
   } else if (c->world == 1) {
@@ -435,6 +440,8 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   a.mc = c->mc;
   a.timeout_ns = (uint64_t)c->p2p_timeout_ms * 1000000ull;
   a.dead_rank = (int32_t)c->emu_dead_rank;
+  a.sig_mode = (int32_t)c->p2p_signal;
+  a.debug = (int32_t)c->p2p_debug;
   c->p2p_seq[ln] += (uint32_t)bk.stages + 2;  // flag values used: seq .. seq + stages + 1
   c->p2p_launches[ln] += 1;
   prof_begin(c, 3, ls);

@@ -153,7 +153,7 @@ int max_ctas_for(const ddp_ctx* c, const Bucket& bk) {
   if (c->emulated || c->peer_emu) {
     // every rank of a launch in one cooperative kernel; in peer emulation the
     // lanes' kernels must also fit side by side (they spin independently)
-    const int e = emulated_max_ctas(bk.algo, c->dtype, (int)bk.params.size(), c->world);
+    const int e = emulated_max_ctas(bk.algo, c->dtype, (int)bk.params.size(), c->world, c->p2p_pull != 0);
     m = std::min(m, std::max(1, e / (c->peer_emu ? lanes_in_use(c) : 1)));
   }
   return std::max(1, m);
@@ -168,6 +168,7 @@ void plan(ddp_ctx* c) {
     bk.algo = resolve_algo(c, bk);
     bk.byte_off = pos;
     pos += align_up(bk.numel * c->esize, 256);
+    if (c->p2p_pull && c->world > 1) continue;  // pull kernels: no staging (second buffer below)
     if (bk.algo == DDP_ALGO_TWOSHOT) l2max = std::max(l2max, align_up(cdiv(bk.numel, c->world), kAlignElems));
     if (bk.algo == DDP_ALGO_ONESHOT && c->world > 1) n1max = std::max(n1max, align_up(bk.numel, kAlignElems));
   }
@@ -177,6 +178,14 @@ void plan(ddp_ctx* c) {
   c->stage1_stride = align_up(n1max * c->esize, 256);
   c->stage1_off = pos;
   pos += c->lanes * 2 * c->world * c->stage1_stride;  // per lane, double-buffered by the lane's launch parity
+  // pull kernels: a second buffer per fused bucket; pass v uses buffer v % 2 (kernels/pull.cu)
+  for (Bucket& bk : c->buckets) {
+    bk.alt_off = bk.byte_off;
+    if (c->p2p_pull && c->world > 1 && (bk.algo == DDP_ALGO_ONESHOT || bk.algo == DDP_ALGO_TWOSHOT)) {
+      bk.alt_off = pos;
+      pos += align_up(bk.numel * c->esize, 256);
+    }
+  }
   // copy-engine buckets: W slots each (dedicated per bucket) + ready/consumed flags
   c->ce_flags_off = pos;
   pos += align_up((int64_t)c->buckets.size() * kMaxWorld * kCeFlagKinds * 4, 256);  // ready, consumed, gathered, bitmap
@@ -332,7 +341,8 @@ ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s, b
 bool is_layout_key(int32_t k) {
   return k == DDP_OPT_P2P_ONESHOT_MAX || k == DDP_OPT_P2P_TWOSHOT_MAX || k == DDP_OPT_ALGO ||
          k == DDP_OPT_FIND_UNUSED || k == DDP_OPT_MULTICAST || k == DDP_OPT_CE_DIRECT_BYTES ||
-         k == DDP_OPT_WIRE_BF16 || k == DDP_OPT_LANES || k == DDP_OPT_PREFER_OVERLAP || k == DDP_OPT_GRAD_VIEW;
+         k == DDP_OPT_WIRE_BF16 || k == DDP_OPT_LANES || k == DDP_OPT_PREFER_OVERLAP || k == DDP_OPT_GRAD_VIEW ||
+         k == DDP_OPT_P2P_PULL;
 }
 
 }  // namespace
@@ -902,6 +912,17 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       if (v < 1) return fail(DDP_ERR_INVALID_ARG, "WAIT_TIMEOUT_MS must be >= 1");
       c->wait_timeout_ms = v;
       return DDP_OK;
+    case DDP_OPT_P2P_PULL:
+      c->p2p_pull = v ? 1 : 0;
+      break;
+    case DDP_OPT_P2P_SIGNAL:
+      if (v < 0 || v > 3) return fail(DDP_ERR_INVALID_ARG, "P2P_SIGNAL must be 0..3");
+      c->p2p_signal = v;
+      return DDP_OK;
+    case DDP_OPT_P2P_DEBUG:
+      if (v < 0 || v > 3) return fail(DDP_ERR_INVALID_ARG, "P2P_DEBUG must be 0..3");
+      c->p2p_debug = v;
+      return DDP_OK;
     case DDP_OPT_EMU_DEAD_RANK:
       if (v < -1 || v >= c->world) return fail(DDP_ERR_INVALID_ARG, "EMU_DEAD_RANK must be -1 or a rank");
       c->emu_dead_rank = v;
@@ -943,6 +964,9 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_P2P_TIMEOUT_MS: *v = c->p2p_timeout_ms; break;
     case DDP_OPT_WAIT_TIMEOUT_MS: *v = c->wait_timeout_ms; break;
     case DDP_OPT_EMU_DEAD_RANK: *v = c->emu_dead_rank; break;
+    case DDP_OPT_P2P_PULL: *v = c->p2p_pull; break;
+    case DDP_OPT_P2P_SIGNAL: *v = c->p2p_signal; break;
+    case DDP_OPT_P2P_DEBUG: *v = c->p2p_debug; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;

@@ -45,6 +45,9 @@ struct P2PLaunch {
   void* mc;                   // NVLS: multicast address of the storage base (NULL otherwise)
   uint64_t timeout_ns;        // bound of every barrier spin (%globaltimer), then *err = 1
   int32_t dead_rank;          // test support (emulation): this rank returns at once, never signals
+  int32_t pull;               // 1: pull kernels (kernels/pull.cu; bucket_byte_off = this pass's buffer)
+  int32_t sig_mode;           // pull kernels: how a flag is published (DDP_OPT_P2P_SIGNAL)
+  int32_t debug;              // measurement only (DDP_OPT_P2P_DEBUG): 1 skip reads, 2 skip pack
 };
 
 // Several buckets launched together at world 1: slot k covers virtual elements
@@ -64,6 +67,9 @@ cudaError_t launch_pack(int dtype, const SlotView& sv, void* bucket, float scale
 cudaError_t launch_unpack(int dtype, const SlotView& sv, const void* bucket, int max_ctas,
                           cudaStream_t s);
 cudaError_t launch_p2p(int algo, int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
+// Pull form of the same two algorithms (kernels/pull.cu): ranks read each other's buffers.
+cudaError_t launch_pull(int algo, int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
+int pull_occupancy(int algo, int dtype, int world, int n_slots);
 // NVLS (NVSwitch multicast) two-shot: pack -> multimem.ld_reduce + multimem.st -> unpack.
 cudaError_t launch_nvls(int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
 // Copy-engine algorithm, SM part.  A list of gradients with their element
@@ -108,6 +114,6 @@ struct UnusedView {
 cudaError_t launch_unused_fixup(int dtype, const UnusedView& uv, const int32_t* global_used, int max_ctas,
                                 cudaStream_t s);
 // Largest number of CTAs per rank an emulated launch of `world` ranks may use.
-int emulated_max_ctas(int algo, int dtype, int n_slots, int world);
+int emulated_max_ctas(int algo, int dtype, int n_slots, int world, bool pull);
 
 }  // namespace b200ddp

@@ -179,6 +179,22 @@ class GradReducer:
             pass
 
 
+def _dense(t: torch.Tensor) -> bool:
+    """t covers exactly numel consecutive elements from its data pointer (any
+    dimension order: contiguous, channels_last, ...).  The average is elementwise,
+    so such a gradient is synchronized as a flat array; every rank's replica has
+    the same layout (same model, same memory format), hence the same element order."""
+    if t.is_contiguous():
+        return True
+    dims = sorted((st, sz) for st, sz in zip(t.stride(), t.size()) if sz != 1)
+    expect = 1
+    for st, sz in dims:
+        if st != expect:
+            return False
+        expect *= sz
+    return True
+
+
 def _tensors(x):
     """Every tensor inside a (nested) forward output: tensors, sequences,
     mappings and dataclass-like objects (e.g. HF ModelOutput)."""
@@ -256,9 +272,15 @@ class DistributedDataParallel(torch.nn.Module):
                                    device=self.params[0].device, options=options)
         self._views = self._make_views()
         if broadcast_parameters and self.reducer.world > 1:
-            states = [t for t in list(module.parameters()) + list(module.buffers()) if t.is_contiguous()]
+            # every parameter and buffer; a non-dense one travels as a contiguous copy
+            # that is copied back (no state may start out different on some rank)
+            states = list(module.parameters()) + list(module.buffers())
             with torch.no_grad():
-                self.reducer.broadcast([t.data for t in states], root=0)
+                bufs = [t.data if _dense(t) else t.data.contiguous() for t in states]
+                self.reducer.broadcast(bufs, root=0)
+                for t, b in zip(states, bufs):
+                    if b.data_ptr() != t.data_ptr():
+                        t.data.copy_(b)
         self._pass_open = False
         self._in_no_sync = False
         self._unused_bufs: Dict[int, torch.Tensor] = {}
@@ -284,8 +306,8 @@ class DistributedDataParallel(torch.nn.Module):
                 # finalize when the autograd engine finishes this backward
                 torch.autograd.Variable._execution_engine.queue_callback(self._finalize)
             g = p.grad
-            if not g.is_contiguous():
-                raise ValueError("gradients must be contiguous")
+            if not _dense(g):
+                raise ValueError("gradients must be dense (contiguous, channels_last, ... : no gaps or overlaps)")
             self.reducer.grad_ready(idx, g)
         return hook
 

@@ -13,6 +13,8 @@ from synth import device as sdev
 TDT = {"fp32": torch.float32, "bf16": torch.bfloat16}
 LDT = {"fp32": L.FP32, "bf16": L.BF16}
 ESZ = {"fp32": 4, "bf16": 2}
+GUARD = 4096          # guard band bytes around each emulated rank's storage
+SENTINEL = -1234.5    # exactly representable in fp32 and bf16
 
 
 def to_np(t: torch.Tensor, dtype: str) -> np.ndarray:
@@ -43,7 +45,7 @@ def run_emulated(numels: Sequence[int], dtype: str, cap: int, W: int, algo: int,
     Returns (inputs[it] as [W, total] cpu tensors, outputs[it], offs)."""
     dev = torch.cuda.current_device()
     offs, total = flat_layout(numels, misalign)
-    big = torch.zeros(W, total, dtype=TDT[dtype], device="cuda")
+    big = torch.full((W, total), SENTINEL, dtype=TDT[dtype], device="cuda")   # gaps keep the sentinel
     ctx = L.ddp_create(numels, LDT[dtype], cap, W, 0)
     ins, outs = [], []
     try:
@@ -51,7 +53,8 @@ def run_emulated(numels: Sequence[int], dtype: str, cap: int, W: int, algo: int,
         for k, v in (options or {}).items():
             L.ddp_set_option(ctx, k, v)
         sb = L.ddp_storage_bytes(ctx)
-        stor = [torch.empty(sb, dtype=torch.uint8, device="cuda") for _ in range(W)]
+        raw = [torch.full((sb + 2 * GUARD,), 0xA5, dtype=torch.uint8, device="cuda") for _ in range(W)]
+        stor = [x[GUARD:GUARD + sb] for x in raw]
         comm = torch.cuda.Stream()
         L.ddp_bind_emulated(ctx, dev, comm.cuda_stream, [s.data_ptr() for s in stor], total * ESZ[dtype])
         ptrs = [big[0, o:].data_ptr() for o in offs]
@@ -68,9 +71,22 @@ def run_emulated(numels: Sequence[int], dtype: str, cap: int, W: int, algo: int,
             outs.append(big.cpu())
         torch.cuda.synchronize()
         L.ddp_check_device_errors(ctx)
+        check_bounds(raw, big, offs, numels)
     finally:
         L.ddp_destroy(ctx)
     return ins, outs, offs
+
+
+def check_bounds(raw, big, offs, numels):
+    """No kernel wrote outside a storage (guard bands) or between the gradients
+    (sentinels): the bounds check this pool offers in place of compute-sanitizer."""
+    torch.cuda.synchronize()
+    for r, x in enumerate(raw):
+        assert bool((x[:GUARD] == 0xA5).all()) and bool((x[-GUARD:] == 0xA5).all()), f"storage guard of rank {r}"
+    mask = torch.ones(big.shape[1], dtype=torch.bool, device=big.device)
+    for o, n in zip(offs, numels):
+        mask[o:o + n] = False
+    assert bool((big[:, mask] == SENTINEL).all()), "a write landed between gradients"
 
 
 def param_slices(t: torch.Tensor, offs, numels, dtype) -> List[List[np.ndarray]]:
@@ -80,9 +96,6 @@ def param_slices(t: torch.Tensor, offs, numels, dtype) -> List[List[np.ndarray]]
 
 
 # ---- peer emulation: one context + one host thread per rank (ddp_bind_peer_emulated) ----
-
-GUARD = 4096          # guard band bytes around each emulated rank's storage
-SENTINEL = -1234.5    # exactly representable in fp32 and bf16
 
 def run_threads(W: int, fn) -> None:
     """fn(rank) on W host threads (the ranks' "processes"); re-raises the first error."""
@@ -196,14 +209,7 @@ class PeerEmu:
     def check_guards(self):
         """No write outside a storage or between the gradients (bounds check in
         place of compute-sanitizer, which this pool does not offer)."""
-        torch.cuda.synchronize()
-        for r, x in enumerate(self._raw):
-            assert bool((x[:GUARD] == 0xA5).all()) and bool((x[-GUARD:] == 0xA5).all()), f"storage guard of rank {r}"
-        mask = torch.ones(self.total, dtype=torch.bool, device="cuda")
-        for o, n in zip(self.offs, self.ns):
-            mask[o:o + n] = False
-        gaps = self.big[:, mask]
-        assert bool((gaps == SENTINEL).all()), "a write landed between gradients"
+        check_bounds(self._raw, self.big, self.offs, self.ns)
 
     def algos(self):
         return [L.ALGO_NAMES[L.ddp_bucket_algo(self.ctx[0], b)] for b in range(L.ddp_num_buckets(self.ctx[0]))]

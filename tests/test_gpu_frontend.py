@@ -155,3 +155,36 @@ def test_world2_broadcast_and_rebuild():
             want = average_bitfaithful([res[r][2][it][1][k].ravel() for r in range(world)], "fp32")
             for r in range(world):
                 assert np.array_equal(res[r][2][it][0][k].ravel(), want), (it, k, r)
+
+
+class _Conv(torch.nn.Module):
+    def __init__(self):
+        super().__init__()
+        self.c1 = torch.nn.Conv2d(3, 16, 3, padding=1)
+        self.c2 = torch.nn.Conv2d(16, 8, 3, padding=1)
+
+    def forward(self, x):
+        return self.c2(torch.relu(self.c1(x)))
+
+
+def test_world1_channels_last_gradients():
+    """A channels_last model: its weight gradients are dense but not contiguous.
+    The hook synchronizes them as flat arrays (the average is elementwise and
+    every replica has the same layout): world 1 leaves them bit-for-bit equal to
+    a plain local backward."""
+    from paper_2006_15704_b200.ddp import DistributedDataParallel
+    torch.manual_seed(0)
+    m = _Conv().cuda().to(memory_format=torch.channels_last)
+    ref = _Conv().cuda().to(memory_format=torch.channels_last)
+    ref.load_state_dict(m.state_dict())
+    ddp = DistributedDataParallel(m, bucket_cap_mb=0.001)
+    try:
+        x = torch.randn(4, 3, 16, 16, device="cuda").to(memory_format=torch.channels_last)
+        ddp(x).square().mean().backward()
+        ref(x).square().mean().backward()
+        torch.cuda.synchronize()
+        assert not m.c1.weight.grad.is_contiguous()          # really exercised the dense path
+        for pm, pr in zip(m.parameters(), ref.parameters()):
+            assert torch.equal(pm.grad, pr.grad)
+    finally:
+        ddp.close()
