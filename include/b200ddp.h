@@ -68,8 +68,9 @@ enum {
   DDP_OPT_OVERLAP = 1,          /* 1 (default): launch buckets from the hooks; 0: launch all at
                                    finalize — the non-overlapped baseline of P:L164-L175 / L399 */
   DDP_OPT_P2P_ONESHOT_MAX = 2,  /* buckets <= this many bytes use the one-shot P2P kernel (default
-                                   1 MiB); larger ones the world-dependent default (world 2: CE,
-                                   world > 2: two-shot) */
+                                   1 MiB); larger ones the world-dependent default (world 2: one-shot
+                                   with the pull kernels (CE with the push kernels), world > 2:
+                                   two-shot) */
   DDP_OPT_P2P_TWOSHOT_MAX = 3,  /* buckets larger than this many bytes use NCCL (default: none) */
   DDP_OPT_COMM_CTAS = 4,        /* max CTAs of a P2P kernel when world > 1 (1..148, default 32);
                                    the last bucket of a pass always runs on 148 */
@@ -115,10 +116,10 @@ enum {
   DDP_OPT_PREFER_OVERLAP = 18,  /* automatic policy for gradients produced by a running backward
                                    (the front end's DistributedDataParallel sets it).  0 (default):
                                    the policy that is fastest when all buckets are ready at once.
-                                   1 (copy engines; chosen for fp32): at world > 2 every bucket but
-                                   the last uses the SM-free copy-engine two-shot (CE2), the last one
-                                   the fastest kernel on every SM.  2 (SM kernels; chosen for bf16):
-                                   at world 2 the one-shot kernel instead of the copy engines.
+                                   1 (copy engines; chosen for fp32): every bucket but the last uses
+                                   an SM-free copy-engine exchange (CE at world 2, CE2 wider), the
+                                   last one the fastest fused kernel on every SM.  2 (SM kernels;
+                                   chosen for bf16): at world 2 the one-shot kernel everywhere.
                                    Layout key */
   DDP_OPT_GRAD_VIEW = 19,       /* gradient-as-bucket-view (§8(f) N-3, zero-copy variant; the
                                    paper's buckets hold copies, Alg. 1 L231-L232 / L246): 1 = the
@@ -159,8 +160,10 @@ enum {
                                    bar.sync, fence.acq_rel.gpu, st.relaxed.sys into each peer; 3:
                                    bar.sync, st.release.gpu of a flag in the OWN storage, which the
                                    peers poll over NVLink (ld.acquire.sys).  Any time */
-  DDP_OPT_P2P_DEBUG = 25        /* measurement only (wrong results!): 1 skips the pull kernels'
-                                   data reads (syncs kept), 2 skips their pack.  Default 0 */
+  DDP_OPT_P2P_DEBUG = 25        /* measurement only: bit 0 skips the pull kernels' data reads and
+                                   bit 1 their pack (syncs kept; wrong results!); bit 2 records a
+                                   %globaltimer trace per CTA into the lane's flag-region scratch
+                                   (kernels/pull.cu trace_point).  Default 0 */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.

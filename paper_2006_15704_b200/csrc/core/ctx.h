@@ -31,6 +31,7 @@ constexpr int64_t kMinChunkElems = 4096;   // smallest per-CTA chunk worth a CTA
 // stage per chunk (one sync for one-shot, two for two-shot); DDP_OPT_P2P_STAGE_BYTES
 // splits chunks for experiments.
 constexpr int64_t kBarrierScratch = 32 * 1024;  // scratch int inside the flags region
+constexpr int64_t kPullStageBytes = 32 * 1024;  // default pipeline stage of the pull kernels
 constexpr int kMaxLanes = 4;
 constexpr int64_t kCeWireAlign = 64;  // elements: wire offsets keep 16-B (and 256-B) alignment
 constexpr int kCeFlagKinds = 4;       // stream-memop flags per bucket: ready, consumed, gathered, bitmap
@@ -166,14 +167,16 @@ struct ddp_ctx {
   void* mc = nullptr;  // NVLS multicast address of the storage base
   int64_t grad_rank_stride = 0;
   std::vector<cudaStream_t> unwaited;  // producer streams since the last event wait
+  cudaStream_t producer = nullptr;     // stream of the most recent ready signal
+  bool from_signal = false;            // device work issued from a ready signal (not finalize)
+  cudaStream_t last_on = nullptr;      // the pass's last bucket ran on this producer stream
+  std::vector<cudaEvent_t> join_ev;    // joins of library streams into last_on
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> stream_events;
   cudaEvent_t comm_done = nullptr;
   uint32_t p2p_seq[kMaxLanes] = {1, 1, 1, 1};
   uint64_t p2p_launches[kMaxLanes] = {};
   cudaStream_t lane_stream[kMaxLanes] = {};  // [0] = comm
   cudaEvent_t lane_done[kMaxLanes] = {};
-  cudaEvent_t lane_tail[kMaxLanes] = {};  // drains the lanes before the last bucket's kernel
-  std::vector<cudaEvent_t> tail_ev;        // ... and the copy-engine streams
   bool lane_used[kMaxLanes] = {};
   uint32_t* err_host = nullptr;
   uint32_t* err_dev = nullptr;

@@ -381,29 +381,38 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   const int ln = (c->emulated || c->world == 1) ? 0 : b % nl;
   cudaStream_t ls = ln == 0 ? c->comm : c->lane_stream[ln];
   if (ln) c->lane_used[ln] = true;
-  if (b == (int)c->buckets.size() - 1 && c->world > 1 && !c->emulated) {
+  const bool last = b == (int)c->buckets.size() - 1 && c->world > 1 && !c->emulated;
+  // The last bucket holds the first-registered parameters: its ready signal is the
+  // end of backward, so nothing is left to overlap with.  Launched from that signal
+  // it runs on the PRODUCER stream itself, after every library stream has been
+  // joined into it: the pass then ends on the producer stream, and the two
+  // cross-stream hops (producer -> comm, comm -> producer) of its sync disappear.
+  const bool on_producer = last && c->from_signal && c->producer && !c->find_unused;
+  auto join = [&](cudaStream_t q, cudaStream_t into, size_t& k) -> ddp_status_t {
+    if (!q || q == into) return DDP_OK;
+    if (k >= c->join_ev.size()) return fail(DDP_ERR_STATE, "join event pool exhausted");
+    CUDA_TRY(c, cudaEventRecord(c->join_ev[k], q));
+    CUDA_TRY(c, cudaStreamWaitEvent(into, c->join_ev[k++], 0));
+    return DDP_OK;
+  };
+  size_t nj = 0;
+  if (last) {
     // The last bucket's kernel uses every SM (max_ctas_for) and spins until the
     // peers arrive.  Everything this rank launched before it must be finished
     // first: the other lanes' spinning kernels (so all of its CTAs can be
     // resident), and the copy-engine paths' kernels of earlier buckets (else
     // they would wait for SMs behind a kernel that waits for peers — measured
     // as a 0.8 ms stall at W=4, profiles/r01_n4.md).
+    if (on_producer) ls = c->producer;
     for (int k = 0; k < nl; ++k) {
-      if (k == ln) continue;
       cudaStream_t ks = k == 0 ? c->comm : c->lane_stream[k];
-      CUDA_TRY(c, cudaEventRecord(c->lane_tail[k], ks));
-      CUDA_TRY(c, cudaStreamWaitEvent(ls, c->lane_tail[k], 0));
+      if (ks == ls && !on_producer) continue;
+      if (ddp_status_t st = join(ks, ls, nj)) return st;
     }
-    size_t q = 0;
-    for (cudaStream_t ks : {c->ce_pack, c->ce_red, c->ce_up}) {
-      if (!ks || q >= c->tail_ev.size()) continue;
-      CUDA_TRY(c, cudaEventRecord(c->tail_ev[q], ks));
-      CUDA_TRY(c, cudaStreamWaitEvent(ls, c->tail_ev[q++], 0));
-    }
-    if (ln != 0 && c->ce_used && q < c->tail_ev.size()) {  // CE copies run on the comm stream
-      CUDA_TRY(c, cudaEventRecord(c->tail_ev[q], c->comm));
-      CUDA_TRY(c, cudaStreamWaitEvent(ls, c->tail_ev[q++], 0));
-    }
+    for (cudaStream_t ks : {c->ce_pack, c->ce_red, c->ce_up})
+      if (ddp_status_t st = join(ks, ls, nj)) return st;
+    if (!on_producer && ln != 0 && c->ce_used)  // CE copies run on the comm stream
+      if (ddp_status_t st = join(c->comm, ls, nj)) return st;
   }
   P2PLaunch a{};
   for (int r = 0; r < c->world; ++r) a.storage[r] = c->storage[r];
@@ -453,6 +462,17 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
     CUDA_TRY(c, launch_p2p(bk.algo, c->dtype, sv, a, ls));
   }
   prof_end(c, ls);
+  if (on_producer) {  // the copy-only streams join after the kernel (they hold no SMs)
+    for (cudaStream_t ks : {c->ce_ag})
+      if (ddp_status_t st = join(ks, ls, nj)) return st;
+    for (cudaStream_t ks : c->ce2_rs)
+      if (ddp_status_t st = join(ks, ls, nj)) return st;
+    for (cudaStream_t ks : c->ce2_ag)
+      if (ddp_status_t st = join(ks, ls, nj)) return st;
+    for (size_t k = 1; k < c->rr_stream.size(); ++k)
+      if (ddp_status_t st = join(c->rr_stream[k], ls, nj)) return st;
+    c->last_on = ls;
+  }
   return DDP_OK;
 }
 
@@ -515,7 +535,7 @@ ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
     // the caller's producer stream is not ordered after its consumer stream
     c->pass_launched = true;
     if (c->comm_done_valid) {
-      for (cudaStream_t q : {c->ce_pack, c->ce_red, c->ce_up, c->ce_ag})
+      for (cudaStream_t q : {c->comm, c->ce_pack, c->ce_red, c->ce_up, c->ce_ag})
         if (q) CUDA_TRY(c, cudaStreamWaitEvent(q, c->comm_done, 0));
       for (cudaStream_t q : c->ce2_rs) CUDA_TRY(c, cudaStreamWaitEvent(q, c->comm_done, 0));
       for (cudaStream_t q : c->ce2_ag) CUDA_TRY(c, cudaStreamWaitEvent(q, c->comm_done, 0));

@@ -106,12 +106,15 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
     // measured at W=4 (profiles/r01_n4.md).  NVLS moves only (1+1/W) S, but the
     // switch path ran at ~0.7x the per-byte rate of SM stores at W=4 (both the
     // fused and the stream-ordered kernel), so it is an option, not a default
-    a = c->world == 2 ? DDP_ALGO_CE : DDP_ALGO_TWOSHOT;
+    // With the pull kernels (round 2) the fused one-shot moves the same S per
+    // direction at W=2 with ONE sync and is faster than the copy engines on the
+    // whole sync (profiles/r02_pull.md), so it is the W=2 choice at every size
+    a = c->world == 2 ? (c->p2p_pull ? DDP_ALGO_ONESHOT : DDP_ALGO_CE) : DDP_ALGO_TWOSHOT;
     // PREFER_OVERLAP (buckets synced while backward still runs): the copy-engine
     // two-shot keeps the SMs with autograd (lowest exposed time at W=4,
     // profiles/r01_n4.md); the last bucket overlaps nothing and keeps the
     // fastest kernel on every SM
-    if (c->prefer_overlap == 1 && c->world > 2 && &bk != &c->buckets.back()) a = DDP_ALGO_CE2;
+    if (c->prefer_overlap == 1 && &bk != &c->buckets.back()) a = c->world > 2 ? DDP_ALGO_CE2 : DDP_ALGO_CE;
     // PREFER_OVERLAP=2 (SM kernels under backward): at world 2 the one-shot kernel
     // instead of the copy engines — measured better for bf16 models (profiles/r01_n2.md)
     if (c->prefer_overlap == 2 && c->world == 2) a = DDP_ALGO_ONESHOT;
@@ -140,7 +143,11 @@ void grid_for(const ddp_ctx* c, Bucket& bk, int max_ctas) {
   bk.shard = L;
   bk.chunk = Q;
   bk.ctas = (int)C;
-  bk.sub = c->stage_bytes > 0 ? std::max<int64_t>(kAlignElems, std::min<int64_t>(Q, c->stage_bytes / c->esize)) : Q;
+  // pipeline stage: DDP_OPT_P2P_STAGE_BYTES, else (pull kernels: the pack warps run
+  // ahead of the read warps stage by stage) kPullStageBytes, else the whole chunk
+  const bool pull = c->p2p_pull && c->world > 1 && bk.algo != DDP_ALGO_NVLS;
+  const int64_t stage = c->stage_bytes > 0 ? c->stage_bytes : pull ? kPullStageBytes : 0;
+  bk.sub = stage > 0 ? std::max<int64_t>(kAlignElems, std::min<int64_t>(Q, stage / c->esize)) : Q;
   bk.stages = (int32_t)cdiv(Q, bk.sub);
 }
 
@@ -277,6 +284,7 @@ ddp_status_t launch_range(ddp_ctx* c, int b0, int b1, int32_t trigger) {
 void open_pass(ddp_ctx* c) {
   c->state = State::IN_PASS;
   c->pass_launched = false;
+  c->last_on = nullptr;
   c->pass_no_sync = c->no_sync;  // reading C-9
   std::fill(c->ready.begin(), c->ready.end(), 0);
   for (size_t b = 0; b < c->buckets.size(); ++b) c->pending[b] = (int32_t)c->buckets[b].params.size();
@@ -329,13 +337,17 @@ ddp_status_t grad_ready_one(ddp_ctx* c, int32_t p, void* grad, cudaStream_t s, b
   c->buckets[b].grads[c->p_slot[p]] = src;
   if (c->pass_no_sync) return DDP_OK;  // hooks disabled
   if (std::find(c->unwaited.begin(), c->unwaited.end(), s) == c->unwaited.end()) c->unwaited.push_back(s);
+  c->producer = s;
   if (!c->overlap) return DDP_OK;
   const int32_t nb = (int32_t)c->buckets.size();
   int32_t e = c->cursor;
   while (e < nb && c->pending[e] == 0) ++e;  // every consecutive ready bucket (C-7)
   const int32_t b0 = c->cursor;
   c->cursor = e;
-  return launch_range(c, b0, e, t);
+  c->from_signal = true;
+  const ddp_status_t st = launch_range(c, b0, e, t);
+  c->from_signal = false;
+  return st;
 }
 
 bool is_layout_key(int32_t k) {
@@ -441,16 +453,13 @@ void ddp_destroy(ddp_ctx_t* c) {
   }
   for (cudaEvent_t e : c->ce_reduced) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ce2_done) cudaEventDestroy(e);
-  for (cudaEvent_t e : c->tail_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : c->join_ev) cudaEventDestroy(e);
   for (int k = 1; k < kMaxLanes; ++k) {
     if (c->lane_stream[k]) {
       if (!c->poisoned) cudaStreamSynchronize(c->lane_stream[k]);
       cudaStreamDestroy(c->lane_stream[k]);
     }
     if (c->lane_done[k]) cudaEventDestroy(c->lane_done[k]);
-  }
-  for (int k = 0; k < kMaxLanes; ++k) {
-    if (c->lane_tail[k]) cudaEventDestroy(c->lane_tail[k]);
   }
   for (cudaEvent_t e : c->ce_packed) cudaEventDestroy(e);
   for (cudaEvent_t e : c->ce_copied) cudaEventDestroy(e);
@@ -555,7 +564,6 @@ ddp_status_t create_side_streams(ddp_ctx* c) {
       CUDA_TRY(c, cudaStreamCreateWithPriority(&c->lane_stream[k], cudaStreamNonBlocking, hi));
       CUDA_TRY(c, cudaEventCreateWithFlags(&c->lane_done[k], cudaEventDisableTiming));
     }
-    for (int k = 0; k < c->lanes; ++k) CUDA_TRY(c, cudaEventCreateWithFlags(&c->lane_tail[k], cudaEventDisableTiming));
   }
   bool any_ce = false;
   for (const Bucket& bk : c->buckets)
@@ -579,11 +587,13 @@ ddp_status_t create_side_streams(ddp_ctx* c) {
     c->ce2_done.assign(2 * nst, nullptr);
     for (auto& e : c->ce2_done) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(c, cudaStreamCreateWithPriority(&c->ce_up, cudaStreamNonBlocking, hi));
-    c->tail_ev.assign(4, nullptr);
-    for (auto& e : c->tail_ev) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     c->ce_reduced.assign(c->buckets.size(), nullptr);
     for (auto& e : c->ce_reduced) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(c, cudaEventCreateWithFlags(&c->ce_red_done, cudaEventDisableTiming));
+  }
+  if (c->world > 1) {  // joins of the library streams before / after the last bucket (exchange.cpp)
+    c->join_ev.assign(48, nullptr);
+    for (auto& e : c->join_ev) CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   if (c->world > 1) {  // copy-engine exchanges and the find_unused bitmap exchange
     cudaDriverEntryPointQueryResult q1, q2;
@@ -759,7 +769,7 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
     const int32_t b0 = c->cursor;  // OVERLAP=0: all launches at finalize, in order
     c->cursor = nb;
     if (ddp_status_t st = launch_range(c, b0, nb, c->n_ready)) return st;
-    if (!c->dry_run) {
+    if (!c->dry_run && !c->last_on) {
       // join the side streams (copy-engine reductions and round-robin NCCL buckets
       // write .grad / scratch there) into the comm stream: one event then covers all
       if (c->ce_used) {
@@ -799,9 +809,16 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
       }
     }
     if (!c->dry_run) {
-      CUDA_TRY(c, cudaEventRecord(c->comm_done, c->comm));
+      // the last bucket ran on its producer stream, after every library stream was
+      // joined into it (exchange.cpp): that stream alone marks the end of the pass
+      cudaStream_t end = c->last_on ? c->last_on : c->comm;
+      CUDA_TRY(c, cudaEventRecord(c->comm_done, end));
       c->comm_done_valid = true;
-      CUDA_TRY(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), c->comm_done, 0));
+      if (static_cast<cudaStream_t>(consumer_stream) != end)
+        CUDA_TRY(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), c->comm_done, 0));
+      c->ce_used = c->ce2_used = false;
+      std::fill(c->lane_used, c->lane_used + kMaxLanes, false);
+      std::fill(c->rr_used.begin(), c->rr_used.end(), 0);
     }
   }
   c->unwaited.clear();
@@ -920,7 +937,7 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       c->p2p_signal = v;
       return DDP_OK;
     case DDP_OPT_P2P_DEBUG:
-      if (v < 0 || v > 3) return fail(DDP_ERR_INVALID_ARG, "P2P_DEBUG must be 0..3");
+      if (v < 0 || v > 7) return fail(DDP_ERR_INVALID_ARG, "P2P_DEBUG must be 0..7");
       c->p2p_debug = v;
       return DDP_OK;
     case DDP_OPT_EMU_DEAD_RANK:

@@ -92,15 +92,16 @@ template <> struct Elem<__nv_bfloat16> {
 // EACH (with SCALE): every operand is scaled and rounded to T BEFORE the sum,
 //   y = RNE_T( sum_k RNE_T(src_k[i] * s) )        (oracle O-3b written out),
 // so raw gradients can be reduced with the 1/W of pack applied on the fly.
+// grp_xfer: the same over a GROUP of nt threads of the CTA (thread index tid in
+// [0, nt)), for warp-specialized kernels; cta_xfer = the whole CTA.
 template <typename T, int NS, int ND, bool SRC_NC, bool SCALE, bool EACH = false, int UF = 0>
-__device__ __forceinline__ void cta_xfer(T* const (&dst)[ND], const T* const (&src)[NS], int64_t n,
-                                         float s) {
+__device__ __forceinline__ void grp_xfer(T* const (&dst)[ND], const T* const (&src)[NS], int64_t n, float s,
+                                         const int tid, const int nt) {
   using E = Elem<T>;
   constexpr int VE = E::VE;
   // 4 vectors per thread in flight for a plain copy: with many small CTAs this
   // measured best on B200 (tools/local_probe.cu; profiles/r01_local_u.md)
   constexpr int U = UF ? UF : NS <= 2 ? 4 : (NS >= 4 ? 1 : 4 / NS);
-  const int tid = threadIdx.x, nt = blockDim.x;
   if (n <= 0) return;
   const uintptr_t a0 = reinterpret_cast<uintptr_t>(dst[0]) & 15;
   uintptr_t mis = 0;
@@ -167,6 +168,12 @@ __device__ __forceinline__ void cta_xfer(T* const (&dst)[ND], const T* const (&s
       if (v + (int64_t)u * nt < nv) vec(v + (int64_t)u * nt, in[u]);
   }
   for (int64_t i = head + nv * VE + tid; i < n; i += nt) scalar(i);
+}
+
+template <typename T, int NS, int ND, bool SRC_NC, bool SCALE, bool EACH = false, int UF = 0>
+__device__ __forceinline__ void cta_xfer(T* const (&dst)[ND], const T* const (&src)[NS], int64_t n,
+                                         float s) {
+  grp_xfer<T, NS, ND, SRC_NC, SCALE, EACH, UF>(dst, src, n, s, (int)threadIdx.x, (int)blockDim.x);
 }
 
 // First slot k with off[k] <= x < off[k+1]  (CTA-uniform binary search).

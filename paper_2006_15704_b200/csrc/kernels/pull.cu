@@ -32,94 +32,145 @@
 //      element) and into .grad;                                  flag kind 1
 //   G  reads chunk c of every other shard j from rank j's buffer (the sums)
 //      straight into .grad.
-// Stages: each CTA chunk is split into `stages` sub-chunks and the phases are
-// software-pipelined (iteration k: P(k), R(k-1), G(k-2)), so local packing of a
-// stage overlaps the NVLink reads of the previous one.
+// Stages + warp specialization: each CTA chunk is split into `stages` sub-chunks;
+// half of the CTA's warps pack stage after stage (P) and publish each, the other
+// half read and reduce one stage behind (R, G), so local packing overlaps the
+// NVLink reads.
 #include "barrier.cuh"
 
 namespace b200ddp {
 
 namespace {
 
-// Publish "this CTA's stores through here are done": kind-0 value v0 and / or
-// kind-1 value v1 (0 = not this time) for the same CTA index of every peer.
-// bar.sync first orders every thread's stores before the publishing thread(s).
-// a.sig_mode (DDP_OPT_P2P_SIGNAL): 0 fence.sc.sys + st.release.sys into each
-// peer; 1 st.release.sys alone; 2 fence.acq_rel.gpu + st.relaxed.sys (the stores
-// being published are LOCAL and already performed at this GPU's L2, which also
-// serves the peers' reads); 3 st.release.gpu into the OWN flag table, polled by
-// the peers over NVLink.
+// Warp specialization: the first kPackThreads threads of a CTA pack stage after
+// stage into the own buffer and publish each one; the other kReadThreads read
+// (over NVLink) and reduce, one stage behind, so local packing overlaps the
+// NVLink reads.  Named barriers: 1 = pack group, 2 = read group.
+constexpr int kPackThreads = kThreads / 4;  // local HBM copies: a quarter of the CTA keeps ahead
+constexpr int kReadThreads = kThreads - kPackThreads;
+
+__device__ __forceinline__ void group_sync(int id, int nt) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nt) : "memory");
+}
+
+// Publish "this group's stores through stage v are done" for the same CTA index
+// of every peer: kind-`kind` value v.  Called by EVERY thread of the group (the
+// group barrier orders all of its stores before the publishing threads).
+// a.sig_mode (DDP_OPT_P2P_SIGNAL): 0 (default) fence.acq_rel.gpu + st.relaxed.sys
+// into each peer: the published stores are LOCAL, so once the gpu-scope fence has
+// them performed at this GPU's L2 — which is also where every peer's read of them
+// is served (peer loads bypass the reader's L2, B300_MICROARCH "NVLink") — the
+// flag store that follows cannot overtake them; 1 fence.sc.sys + st.release.sys
+// (the formal system-scope release; measured ~7 us per publish, profiles/r02_pull.md);
+// 2 st.release.sys alone; 3 st.release.gpu into the OWN flag table, polled by the
+// peers over NVLink.  `smem` (optional): the group's progress for the other group
+// of this CTA, written after the fence.
 template <int W>
-__device__ __forceinline__ void pull_signal(const P2PLaunch& a, int r, uint32_t v0, uint32_t v1) {
-  __syncthreads();
-  const int t = threadIdx.x;
+__device__ __forceinline__ void group_publish(const P2PLaunch& a, int r, int kind, uint32_t v, int bar_id, int gt,
+                                              int nt, volatile uint32_t* smem, uint32_t smem_v) {
+  group_sync(bar_id, nt);
   if (a.sig_mode == 3) {
-    if (t == 0) {
-      if (v0) {
-        uint32_t* f = flag_ptr(a.storage[r], a.flags_byte_off, 0, blockIdx.x, r);
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v0) : "memory");
-      }
-      if (v1) {
-        uint32_t* f = flag_ptr(a.storage[r], a.flags_byte_off, 1, blockIdx.x, r);
-        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v1) : "memory");
-      }
+    if (gt == 0) {
+      uint32_t* f = flag_ptr(a.storage[r], a.flags_byte_off, kind, blockIdx.x, r);
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+      if (smem) *smem = smem_v;
     }
     return;
   }
-  if (t < W && t != r) {
-    if (a.sig_mode == 0) __threadfence_system();
-    if (a.sig_mode == 2) asm volatile("fence.acq_rel.gpu;" ::: "memory");
-    for (int kind = 0; kind < 2; ++kind) {
-      const uint32_t v = kind ? v1 : v0;
-      if (!v) continue;
-      uint32_t* f = flag_ptr(a.storage[t], a.flags_byte_off, kind, blockIdx.x, r);
-      if (a.sig_mode == 2) asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+  if (gt < W && (gt != r || smem)) {
+    if (a.sig_mode == 1) __threadfence_system();
+    else if (a.sig_mode == 0) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+    if (gt != r) {
+      uint32_t* f = flag_ptr(a.storage[gt], a.flags_byte_off, kind, blockIdx.x, r);
+      if (a.sig_mode == 0) asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
       else asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+    } else {
+      __threadfence();  // own group's progress for the other group (gpu scope suffices: same SM)
+      *smem = smem_v;
     }
   }
 }
 
-// Wait until every peer's same-index CTA has published >= val (bounded spin);
-// sig_mode 3 polls the peers' own flag tables over NVLink.
+// Wait (whole group) until every peer's same-index CTA has published kind >= val
+// and, if `smem`, this CTA's other group has reached smem_v.  Bounded spin.
 template <int W>
-__device__ __forceinline__ void pull_wait(const P2PLaunch& a, int r, int kind, uint32_t val) {
-  const int t = threadIdx.x;
-  if (t < W && t != r) {
-    const uint32_t* f = a.sig_mode == 3 ? flag_ptr(a.storage[t], a.flags_byte_off, kind, blockIdx.x, t)
-                                        : flag_ptr(a.storage[r], a.flags_byte_off, kind, blockIdx.x, t);
+__device__ __forceinline__ void group_wait(const P2PLaunch& a, int r, int kind, uint32_t val, int bar_id, int gt,
+                                           int nt, volatile uint32_t* smem, uint32_t smem_v) {
+  if (gt < W) {
     const uint64_t t0 = globaltimer();
-    while (true) {
-      uint32_t v;
-      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-      if ((int32_t)(v - val) >= 0) break;
-      if (globaltimer() - t0 > a.timeout_ns) {
-        atomicExch(a.err, 1u);
-        break;
+    if (gt != r) {
+      const uint32_t* f = a.sig_mode == 3 ? flag_ptr(a.storage[gt], a.flags_byte_off, kind, blockIdx.x, gt)
+                                          : flag_ptr(a.storage[r], a.flags_byte_off, kind, blockIdx.x, gt);
+      while (true) {
+        uint32_t v;
+        asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if ((int32_t)(v - val) >= 0) break;
+        if (globaltimer() - t0 > a.timeout_ns) {
+          atomicExch(a.err, 1u);
+          break;
+        }
       }
+    } else if (smem) {
+      while ((int32_t)(*smem - smem_v) < 0) {
+        if (globaltimer() - t0 > a.timeout_ns) {
+          atomicExch(a.err, 1u);
+          break;
+        }
+      }
+      __threadfence_block();
     }
   }
-  __syncthreads();
+  group_sync(bar_id, nt);
 }
 
-// grad(x) = RNE( sum_{k<NS} src_k[x - base] ) for x in [lo, hi) (rank order), also
-// written to extra[x - base] when EXTRA (the two-shot's own shard, in place).
-template <typename T, int NS, bool EXTRA, int MAXS>
-__device__ __forceinline__ void walk_sum(const SlotArgs<MAXS>& sa, int64_t lo, int64_t hi,
-                                         const T* const (&srcb)[NS], T* extra, int64_t base, int64_t gstride) {
+// Measurement only (DDP_OPT_P2P_DEBUG bit 2 = 4): one thread per CTA records
+// %globaltimer at point i (0 entry, 1 stage 0 packed, 2 stage 0 published,
+// 3 stage 0 seen from every peer, 4 stage 0 read, 5 last stage read, 6 end) into
+// uint64 [kMaxCtas][8] at byte 40 KiB of the lane's flag region (scratch).
+__device__ __forceinline__ void trace_point(const P2PLaunch& a, int r, int i, bool who) {
+  if ((a.debug & 4) && who)
+    reinterpret_cast<uint64_t*>(static_cast<char*>(a.storage[r]) + a.flags_byte_off + 40 * 1024)[blockIdx.x * 8 + i] =
+        globaltimer();
+}
+
+// Pack the bucket range [lo, hi) from the gradients (x s) into dst[x], by a group.
+template <typename T, int MAXS>
+__device__ __forceinline__ void grp_pack(const SlotArgs<MAXS>& sa, int64_t lo, int64_t hi, T* dst, float s,
+                                         int64_t gstride, int gt, int nt) {
   if (lo >= hi) return;
+  for (int k = find_slot(sa, lo); k < sa.n && lo < hi; ++k) {
+    const int64_t s0 = sa.off[k], e = min(hi, sa.off[k + 1]);
+    if (e <= lo) continue;
+    const T* g = reinterpret_cast<const T*>(static_cast<const char*>(sa.grad[k]) + gstride) + (lo - s0);
+    T* d[1] = {dst + lo};
+    const T* sp[1] = {g};
+    grp_xfer<T, 1, 1, true, true, false, 8>(d, sp, e - lo, s, gt, nt);
+    lo = e;
+  }
+}
+
+// grad(x) = RNE( sum_{k<NS} src_k[x] ) for x in [lo, hi) (rank order), by a group;
+// also written to extra[x] when EXTRA (the two-shot's own shard, in place).
+template <typename T, int NS, bool EXTRA, int MAXS>
+__device__ __forceinline__ void grp_sum(const SlotArgs<MAXS>& sa, int64_t lo, int64_t hi,
+                                        const T* const (&srcb)[NS], T* extra, int64_t gstride, int gt, int nt) {
+  if (lo >= hi) return;
+  // remote loads are latency-bound: keep ~16 16-B loads in flight per thread
+  // (EXTRA, the two-shot's reduce with two destinations: fewer, to stay in 128 registers)
+  constexpr int UF = EXTRA ? (NS <= 2 ? 4 : NS <= 4 ? 3 : NS <= 6 ? 2 : 1) : (NS <= 2 ? 8 : NS <= 4 ? 4 : 2);
   for (int k = find_slot(sa, lo); k < sa.n && lo < hi; ++k) {
     const int64_t s0 = sa.off[k], e = min(hi, sa.off[k + 1]);
     if (e <= lo) continue;
     T* g = reinterpret_cast<T*>(static_cast<char*>(sa.grad[k]) + gstride) + (lo - s0);
     const T* sp[NS];
 #pragma unroll
-    for (int j = 0; j < NS; ++j) sp[j] = srcb[j] + (lo - base);
+    for (int j = 0; j < NS; ++j) sp[j] = srcb[j] + lo;
     if (EXTRA) {
-      T* d[2] = {g, extra + (lo - base)};
-      cta_xfer<T, NS, 2, false, false>(d, sp, e - lo, 1.0f);
+      T* d[2] = {g, extra + lo};
+      grp_xfer<T, NS, 2, false, false, false, UF>(d, sp, e - lo, 1.0f, gt, nt);
     } else {
       T* d[1] = {g};
-      cta_xfer<T, NS, 1, false, false>(d, sp, e - lo, 1.0f);
+      grp_xfer<T, NS, 1, false, false, false, UF>(d, sp, e - lo, 1.0f, gt, nt);
     }
     lo = e;
   }
@@ -138,20 +189,40 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
   for (int q = 0; q < W; ++q) buf[q] = at<T>(a.storage[q], a.bucket_byte_off);
   const int K = a.stages;
+  __shared__ uint32_t packed;  // stages packed by this CTA's pack group
+  if (threadIdx.x == 0) packed = 0;
+  __syncthreads();
+  trace_point(a, r, 0, threadIdx.x == 0);
+  auto stage = [&](int k, int64_t& lo, int64_t& hi) {
+    lo = min(lo0 + (int64_t)k * a.sub, hi0);
+    hi = min(lo + a.sub, hi0);
+  };
+  if (threadIdx.x < kPackThreads) {  // P: pack + scale every stage into the own buffer, publish each
+    const int gt = threadIdx.x;
 #pragma unroll 1
-  for (int k = 0; k <= K; ++k) {
-    if (k < K) {  // P: pack + scale stage k into the own buffer, then publish it
-      const int64_t lo = min(lo0 + (int64_t)k * a.sub, hi0), hi = min(lo + a.sub, hi0);
-      T* d[1] = {own};
-      if (!(a.debug & 2)) walk_pack<T, 1, MAXS>(sa, lo, hi, d, 0, a.scale, gstride);
-      pull_signal<W>(a, r, a.seq + (uint32_t)(k + 1), 0);
+    for (int k = 0; k < K; ++k) {
+      int64_t lo, hi;
+      stage(k, lo, hi);
+      if (!(a.debug & 2)) grp_pack<T, MAXS>(sa, lo, hi, own, a.scale, gstride, gt, kPackThreads);
+      if (k == 0) trace_point(a, r, 1, gt == 0);
+      group_publish<W>(a, r, 0, a.seq + (uint32_t)(k + 1), 1, gt, kPackThreads, &packed, (uint32_t)(k + 1));
+      if (k == 0) trace_point(a, r, 2, gt == 0);
     }
-    if (k >= 1) {  // R: stage k-1 of every rank's buffer -> rank-order sum -> .grad
-      pull_wait<W>(a, r, 0, a.seq + (uint32_t)k);
-      const int64_t lo = min(lo0 + (int64_t)(k - 1) * a.sub, hi0), hi = min(lo + a.sub, hi0);
-      if (!(a.debug & 1)) walk_sum<T, W, false, MAXS>(sa, lo, hi, buf, nullptr, 0, gstride);
+  } else {  // R: each stage of every rank's buffer -> rank-order sum -> .grad
+    const int gt = threadIdx.x - kPackThreads;
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+      group_wait<W>(a, r, 0, a.seq + (uint32_t)(k + 1), 2, gt, kReadThreads, &packed, (uint32_t)(k + 1));
+      if (k == 0) trace_point(a, r, 3, gt == 0);
+      int64_t lo, hi;
+      stage(k, lo, hi);
+      if (!(a.debug & 1)) grp_sum<T, W, false, MAXS>(sa, lo, hi, buf, nullptr, gstride, gt, kReadThreads);
+      if (k == 0) trace_point(a, r, 4, gt == 0);
     }
+    trace_point(a, r, 5, gt == 0);
   }
+  __syncthreads();
+  trace_point(a, r, 6, threadIdx.x == 0);
 }
 
 template <typename T, int W, int MAXS>
@@ -173,39 +244,53 @@ __global__ void __launch_bounds__(kThreads, 1)
   const T* buf[W];
 #pragma unroll
   for (int q = 0; q < W; ++q) buf[q] = at<T>(a.storage[q], a.bucket_byte_off);
-
+  __shared__ uint32_t packed;
+  if (threadIdx.x == 0) packed = 0;
+  __syncthreads();
+  trace_point(a, r, 0, threadIdx.x == 0);
+  if (threadIdx.x < kPackThreads) {  // P: pack + scale stage k of chunk c of every shard, publish (kind 0)
+    const int gt = threadIdx.x;
 #pragma unroll 1
-  for (int k = 0; k <= K + 1; ++k) {
-    if (k < K) {  // P: pack + scale stage k of chunk c of every shard into the own buffer
-      T* d[1] = {own};
+    for (int k = 0; k < K; ++k) {
 #pragma unroll 1
       for (int j = 0; j < W; ++j) {
         int64_t lo, hi;
-        rng(j, k, lo, hi);
-        if (!(a.debug & 2)) walk_pack<T, 1, MAXS>(sa, lo, hi, d, 0, a.scale, gstride);
+        rng((r + 1 + j) % W, k, lo, hi);  // own shard last: the peers need theirs first
+        if (!(a.debug & 2)) grp_pack<T, MAXS>(sa, lo, hi, own, a.scale, gstride, gt, kPackThreads);
       }
+      if (k == 0) trace_point(a, r, 1, gt == 0);
+      group_publish<W>(a, r, 0, a.seq + (uint32_t)(k + 1), 1, gt, kPackThreads, &packed, (uint32_t)(k + 1));
+      if (k == 0) trace_point(a, r, 2, gt == 0);
     }
-    if (k >= 1 && k <= K) {  // R: own shard, stage k-1: sum over the W buffers -> own buffer + .grad
-      pull_wait<W>(a, r, 0, a.seq + (uint32_t)k);
-      int64_t lo, hi;
-      rng(r, k - 1, lo, hi);
-      if (!(a.debug & 1)) walk_sum<T, W, true, MAXS>(sa, lo, hi, buf, own, 0, gstride);
-    }
-    // publish: "packed through stage k" (kind 0) and "reduced through stage k-1" (kind 1);
-    // one CTA barrier + one release covers both (local stores only)
-    if (k <= K) pull_signal<W>(a, r, k < K ? a.seq + (uint32_t)(k + 1) : 0u, k >= 1 ? a.seq + (uint32_t)k : 0u);
-    if (k >= 2) {  // G: every other shard j, stage k-2, from rank j's buffer -> .grad
-      pull_wait<W>(a, r, 1, a.seq + (uint32_t)(k - 1));
+  } else {
+    const int gt = threadIdx.x - kPackThreads;
 #pragma unroll 1
-      for (int i = 1; i < W; ++i) {
-        const int j = (r + i) % W;
+    for (int k = 0; k <= K; ++k) {
+      if (k < K) {  // R: own shard, stage k: sum over the W buffers -> own buffer + .grad; publish (kind 1)
+        group_wait<W>(a, r, 0, a.seq + (uint32_t)(k + 1), 2, gt, kReadThreads, &packed, (uint32_t)(k + 1));
+        if (k == 0) trace_point(a, r, 3, gt == 0);
         int64_t lo, hi;
-        rng(j, k - 2, lo, hi);
-        const T* src[1] = {buf[j]};
-        if (!(a.debug & 1)) walk_sum<T, 1, false, MAXS>(sa, lo, hi, src, nullptr, 0, gstride);
+        rng(r, k, lo, hi);
+        if (!(a.debug & 1)) grp_sum<T, W, true, MAXS>(sa, lo, hi, buf, own, gstride, gt, kReadThreads);
+        if (k == 0) trace_point(a, r, 4, gt == 0);
+        group_publish<W>(a, r, 1, a.seq + (uint32_t)(k + 1), 2, gt, kReadThreads, nullptr, 0);
+      }
+      if (k >= 1) {  // G: every other shard j, stage k-1, from rank j's buffer (its sums) -> .grad
+        group_wait<W>(a, r, 1, a.seq + (uint32_t)k, 2, gt, kReadThreads, nullptr, 0);
+#pragma unroll 1
+        for (int i = 1; i < W; ++i) {
+          const int j = (r + i) % W;
+          int64_t lo, hi;
+          rng(j, k - 1, lo, hi);
+          const T* src[1] = {buf[j]};
+          if (!(a.debug & 1)) grp_sum<T, 1, false, MAXS>(sa, lo, hi, src, nullptr, gstride, gt, kReadThreads);
+        }
       }
     }
+    trace_point(a, r, 5, gt == 0);
   }
+  __syncthreads();
+  trace_point(a, r, 6, threadIdx.x == 0);
 }
 
 template <int MAXS>

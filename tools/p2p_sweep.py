@@ -52,10 +52,12 @@ def main():
             ("twoshot push", {O.OPT_ALGO: A.ALGO_TWOSHOT, O.OPT_P2P_PULL: 0}),
         ] + [(f"{alg} pull sig{m} stage{st}", {O.OPT_ALGO: getattr(A, "ALGO_" + alg.upper()), O.OPT_P2P_SIGNAL: m,
                                                O.OPT_P2P_STAGE_BYTES: st << 10})
-             for alg in ("oneshot", "twoshot") for m in (0, 1, 2, 3) for st in (0, 64)]
+             for alg in ("oneshot", "twoshot") for m in (0, 1, 3) for st in (16, 32, 64, 1 << 20)]
         + [(f"{alg} pull debug{d}", {O.OPT_ALGO: getattr(A, "ALGO_" + alg.upper()), O.OPT_P2P_DEBUG: d})
            for alg in ("oneshot", "twoshot") for d in (1, 2, 3)]
-        + [("ce", {O.OPT_ALGO: A.ALGO_CE})],
+        + [("ce", {O.OPT_ALGO: A.ALGO_CE}), ("ce2", {O.OPT_ALGO: A.ALGO_CE2}), ("nccl", {O.OPT_ALGO: A.ALGO_NCCL})],
+        "quick": [(f"{alg} pull", {O.OPT_ALGO: getattr(A, "ALGO_" + alg.upper())}) for alg in ("oneshot", "twoshot")]
+        + [("ce", {O.OPT_ALGO: A.ALGO_CE}), ("ce2", {O.OPT_ALGO: A.ALGO_CE2}), ("nccl", {O.OPT_ALGO: A.ALGO_NCCL})],
     }[a.sets]
 
     def tmax(x):
