@@ -62,6 +62,7 @@ def parse():
                     help="communication streams at the highest priority (default: lowest)")
     ap.add_argument("--lanes", type=int, default=0, help="P2P/NVLS kernel lanes (streams)")
     ap.add_argument("--p2p-push", action="store_true", help="round-1 push kernels instead of the pull kernels")
+    ap.add_argument("--last-on-lane", action="store_true", help="DDP_OPT_LAST_ON_PRODUCER=0")
     ap.add_argument("--wire-bf16", action="store_true", help="N-3: fp32 gradients travel as bf16 (CE exchange)")
     ap.add_argument("--grad-view", action="store_true",
                     help="N-3 zero-copy: gradients live in their bucket slots (in-place NCCL, no pack/unpack)")
@@ -242,6 +243,8 @@ def run_ours(a):
         opts[L.OPT_LANES] = a.lanes
     if a.p2p_push:
         opts[L.OPT_P2P_PULL] = 0
+    if a.last_on_lane:
+        opts[L.OPT_LAST_ON_PRODUCER] = 0
     if a.wire_bf16:
         opts[L.OPT_WIRE_BF16] = 1
     if a.grad_view:
@@ -897,6 +900,8 @@ def _opts(a):
         o[L.OPT_LANES] = a.lanes
     if a.p2p_push:
         o[L.OPT_P2P_PULL] = 0
+    if a.last_on_lane:
+        o[L.OPT_LAST_ON_PRODUCER] = 0
     if a.wire_bf16:
         o[L.OPT_WIRE_BF16] = 1
     if a.grad_view:
@@ -956,7 +961,8 @@ def allreduce_sweep(a, rank, world, local, dev, opts):
     esize = 4 if a.dtype == "fp32" else 2
     stream = torch.cuda.current_stream(dev)
     algos = [L.ALGO_AUTO, L.ALGO_NCCL, L.ALGO_ONESHOT, L.ALGO_TWOSHOT] + (
-        [L.ALGO_CE, L.ALGO_NVLS, L.ALGO_PUSH] if world > 1 else [])
+        [L.ALGO_CE, L.ALGO_CE2, L.ALGO_NVLS, L.ALGO_PUSH] if world > 1 else [])
+    nccl_algo = os.environ.get("NCCL_ALGO", "default")
     sizes = [4 << 10, 64 << 10, 256 << 10, 1 << 20, 4 << 20, 16 << 20, 25 << 20, 64 << 20, 256 << 20]
     res = []
 
@@ -992,9 +998,10 @@ def allreduce_sweep(a, rank, world, local, dev, opts):
             def one():
                 red.grad_ready(0, g, stream)
                 red.finalize(stream)
-            t = time_it(one, 20 if S <= (64 << 20) else 5)
+            t = time_it(one, 100 if S <= (64 << 20) else 10)
             bw = S / (t * 1e-3) * 2 * (world - 1) / world / 1e9 if world > 1 else None
             res.append({"mode": "allreduce-sweep", "n_gpus": world, "dtype": a.dtype, "bytes": S,
+                        "nccl_algo": nccl_algo, "reps": 100 if S <= (64 << 20) else 10,
                         "algo": red.bucket_algos()[0], "forced": L.ALGO_NAMES[algo] if algo else "auto",
                         "ms": t, "busbw_gbs": bw, "algbw_gbs": S / (t * 1e-3) / 1e9,
                         "includes": "pack x1/W + allreduce + unpack (fused kernel for P2P)"})

@@ -154,16 +154,21 @@ enum {
                                    before each flag drains local stores only, .grad is written by
                                    the reads (no unpack pass, no closing barrier).  0: push form
                                    (remote stores into per-lane staging, round 1).  Layout key */
-  DDP_OPT_P2P_SIGNAL = 24,      /* pull kernels, measurement knob: how "my stores are done" is
-                                   published.  0 (default): bar.sync, fence.sc.sys, st.release.sys of
-                                   the flag into each peer; 1: bar.sync, st.release.sys only; 2:
-                                   bar.sync, fence.acq_rel.gpu, st.relaxed.sys into each peer; 3:
-                                   bar.sync, st.release.gpu of a flag in the OWN storage, which the
-                                   peers poll over NVLink (ld.acquire.sys).  Any time */
-  DDP_OPT_P2P_DEBUG = 25        /* measurement only: bit 0 skips the pull kernels' data reads and
+  DDP_OPT_P2P_SIGNAL = 24,      /* pull kernels: how a group publishes "my (local) stores are done"
+                                   after its named barrier.  0 (default): fence.acq_rel.gpu +
+                                   st.relaxed.sys of the flag into each peer (reading A-1);
+                                   1: fence.sc.sys + st.release.sys (the formal system-scope release,
+                                   5-8 us per publish); 2: st.release.sys alone; 3: st.release.gpu of
+                                   a flag in the OWN storage, polled by the peers over NVLink
+                                   (ld.acquire.sys).  Any time */
+  DDP_OPT_P2P_DEBUG = 25,       /* measurement only: bit 0 skips the pull kernels' data reads and
                                    bit 1 their pack (syncs kept; wrong results!); bit 2 records a
                                    %globaltimer trace per CTA into the lane's flag-region scratch
                                    (kernels/pull.cu trace_point).  Default 0 */
+  DDP_OPT_LAST_ON_PRODUCER = 26 /* 1 (default): the pass's last bucket, when fused and launched from
+                                   a ready signal, runs on that signal's producer stream after every
+                                   library stream is joined into it (the pass then ends there);
+                                   0: on its lane like the others.  Any time */
 };
 
 /* Algorithm codes reported by ddp_bucket_algo / used by DDP_OPT_ALGO.

@@ -26,7 +26,7 @@ OPT_OVERLAP, OPT_P2P_ONESHOT_MAX, OPT_P2P_TWOSHOT_MAX, OPT_COMM_CTAS, OPT_DRY_RU
     OPT_ALGO, OPT_PACK_CTAS, OPT_P2P_STAGE_BYTES, OPT_FIND_UNUSED, OPT_MULTICAST, OPT_CE_STREAMS, \
     OPT_NCCL_COMMS, OPT_CE_DIRECT_BYTES, OPT_WIRE_BF16, OPT_LANES, OPT_LOW_PRIORITY, \
     OPT_PREFER_OVERLAP, OPT_GRAD_VIEW, OPT_P2P_TIMEOUT_MS, OPT_WAIT_TIMEOUT_MS, OPT_EMU_DEAD_RANK, \
-    OPT_P2P_PULL, OPT_P2P_SIGNAL, OPT_P2P_DEBUG = range(1, 26)
+    OPT_P2P_PULL, OPT_P2P_SIGNAL, OPT_P2P_DEBUG, OPT_LAST_ON_PRODUCER = range(1, 27)
 ALGO_AUTO, ALGO_NCCL, ALGO_ONESHOT, ALGO_TWOSHOT, ALGO_CE, ALGO_NVLS, ALGO_PUSH, ALGO_CE2 = range(8)
 ALGO_NAMES = {ALGO_NCCL: "nccl", ALGO_ONESHOT: "oneshot", ALGO_TWOSHOT: "twoshot", ALGO_CE: "ce",
               ALGO_NVLS: "nvls", ALGO_PUSH: "push", ALGO_CE2: "ce2"}

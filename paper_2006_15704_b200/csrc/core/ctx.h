@@ -106,6 +106,7 @@ struct ddp_ctx {
   int64_t p2p_pull = 1;             // fused P2P kernels: 1 pull (kernels/pull.cu), 0 push (kernels/p2p.cu)
   int64_t p2p_signal = 0;           // pull kernels: flag publication mode (DDP_OPT_P2P_SIGNAL)
   int64_t p2p_debug = 0;            // measurement only: skip data phases (DDP_OPT_P2P_DEBUG)
+  int64_t last_on_producer = 1;     // the pass's last fused bucket runs on its producer stream
   // symmetric storage layout (bytes)
   int64_t flags_off = 0, buckets_off = 0, stage2_off = 0, stage2_stride = 0, stage1_off = 0,
           stage1_stride = 0, ce_flags_off = 0, bitmap_off = 0, bitmap_stride = 0, global_off = 0,

@@ -387,7 +387,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   // it runs on the PRODUCER stream itself, after every library stream has been
   // joined into it: the pass then ends on the producer stream, and the two
   // cross-stream hops (producer -> comm, comm -> producer) of its sync disappear.
-  const bool on_producer = last && c->from_signal && c->producer && !c->find_unused;
+  const bool on_producer = last && c->last_on_producer && c->from_signal && c->producer && !c->find_unused;
   auto join = [&](cudaStream_t q, cudaStream_t into, size_t& k) -> ddp_status_t {
     if (!q || q == into) return DDP_OK;
     if (k >= c->join_ev.size()) return fail(DDP_ERR_STATE, "join event pool exhausted");

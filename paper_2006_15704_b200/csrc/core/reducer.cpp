@@ -936,6 +936,9 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       if (v < 0 || v > 3) return fail(DDP_ERR_INVALID_ARG, "P2P_SIGNAL must be 0..3");
       c->p2p_signal = v;
       return DDP_OK;
+    case DDP_OPT_LAST_ON_PRODUCER:
+      c->last_on_producer = v ? 1 : 0;
+      return DDP_OK;
     case DDP_OPT_P2P_DEBUG:
       if (v < 0 || v > 7) return fail(DDP_ERR_INVALID_ARG, "P2P_DEBUG must be 0..7");
       c->p2p_debug = v;
@@ -984,6 +987,7 @@ ddp_status_t ddp_get_option(const ddp_ctx_t* c, int32_t key, int64_t* v) {
     case DDP_OPT_P2P_PULL: *v = c->p2p_pull; break;
     case DDP_OPT_P2P_SIGNAL: *v = c->p2p_signal; break;
     case DDP_OPT_P2P_DEBUG: *v = c->p2p_debug; break;
+    case DDP_OPT_LAST_ON_PRODUCER: *v = c->last_on_producer; break;
     default: return fail(DDP_ERR_INVALID_ARG, "unknown option key");
   }
   return DDP_OK;
