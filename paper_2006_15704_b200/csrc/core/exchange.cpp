@@ -450,6 +450,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   a.timeout_ns = (uint64_t)c->p2p_timeout_ms * 1000000ull;
   a.dead_rank = (int32_t)c->emu_dead_rank;
   a.sig_mode = (int32_t)c->p2p_signal;
+  a.pack_threads = bk.ctas >= 96 ? kThreads / 4 : kThreads / 2;
   a.debug = (int32_t)c->p2p_debug;
   c->p2p_seq[ln] += (uint32_t)bk.stages + 2;  // flag values used: seq .. seq + stages + 1
   c->p2p_launches[ln] += 1;

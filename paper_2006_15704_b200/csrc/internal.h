@@ -48,6 +48,7 @@ struct P2PLaunch {
   int32_t pull;               // 1: pull kernels (kernels/pull.cu; bucket_byte_off = this pass's buffer)
   int32_t sig_mode;           // pull kernels: how a flag is published (DDP_OPT_P2P_SIGNAL)
   int32_t debug;              // measurement only (DDP_OPT_P2P_DEBUG): 1 skip reads, 2 skip pack
+  int32_t pack_threads;       // pull kernels: threads of the pack group (multiple of 32, < kThreads)
 };
 
 // Several buckets launched together at world 1: slot k covers virtual elements

@@ -42,12 +42,13 @@ namespace b200ddp {
 
 namespace {
 
-// Warp specialization: the first kPackThreads threads of a CTA pack stage after
-// stage into the own buffer and publish each one; the other kReadThreads read
-// (over NVLink) and reduce, one stage behind, so local packing overlaps the
-// NVLink reads.  Named barriers: 1 = pack group, 2 = read group.
-constexpr int kPackThreads = kThreads / 4;  // local HBM copies: a quarter of the CTA keeps ahead
-constexpr int kReadThreads = kThreads - kPackThreads;
+// Warp specialization: the first a.pack_threads threads of a CTA pack stage after
+// stage into the own buffer and publish each one; the other kThreads -
+// a.pack_threads read (over NVLink) and reduce, one stage behind, so local packing
+// overlaps the NVLink reads.  Named barriers: 1 = pack group, 2 = read group.
+// The host picks the split: a quarter of the CTA packs when the grid covers the
+// SMs (each CTA's chunk is small), half when it is capped (COMM_CTAS): there the
+// pack of a large per-CTA chunk would otherwise hold the reads back.
 
 __device__ __forceinline__ void group_sync(int id, int nt) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nt) : "memory");
@@ -134,7 +135,7 @@ __device__ __forceinline__ void trace_point(const P2PLaunch& a, int r, int i, bo
 }
 
 // Pack the bucket range [lo, hi) from the gradients (x s) into dst[x], by a group.
-template <typename T, int MAXS>
+template <typename T, int MAXS, int U>
 __device__ __forceinline__ void grp_pack(const SlotArgs<MAXS>& sa, int64_t lo, int64_t hi, T* dst, float s,
                                          int64_t gstride, int gt, int nt) {
   if (lo >= hi) return;
@@ -144,7 +145,7 @@ __device__ __forceinline__ void grp_pack(const SlotArgs<MAXS>& sa, int64_t lo, i
     const T* g = reinterpret_cast<const T*>(static_cast<const char*>(sa.grad[k]) + gstride) + (lo - s0);
     T* d[1] = {dst + lo};
     const T* sp[1] = {g};
-    grp_xfer<T, 1, 1, true, true, false, 8>(d, sp, e - lo, s, gt, nt);
+    grp_xfer<T, 1, 1, true, true, false, U>(d, sp, e - lo, s, gt, nt);
     lo = e;
   }
 }
@@ -197,26 +198,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     lo = min(lo0 + (int64_t)k * a.sub, hi0);
     hi = min(lo + a.sub, hi0);
   };
-  if (threadIdx.x < kPackThreads) {  // P: pack + scale every stage into the own buffer, publish each
+  const int np = a.pack_threads, nr = kThreads - np;
+  if (threadIdx.x < np) {  // P: pack + scale every stage into the own buffer, publish each
     const int gt = threadIdx.x;
 #pragma unroll 1
     for (int k = 0; k < K; ++k) {
       int64_t lo, hi;
       stage(k, lo, hi);
-      if (!(a.debug & 2)) grp_pack<T, MAXS>(sa, lo, hi, own, a.scale, gstride, gt, kPackThreads);
+      if (!(a.debug & 2)) grp_pack<T, MAXS, 16>(sa, lo, hi, own, a.scale, gstride, gt, np);
       if (k == 0) trace_point(a, r, 1, gt == 0);
-      group_publish<W>(a, r, 0, a.seq + (uint32_t)(k + 1), 1, gt, kPackThreads, &packed, (uint32_t)(k + 1));
+      group_publish<W>(a, r, 0, a.seq + (uint32_t)(k + 1), 1, gt, np, &packed, (uint32_t)(k + 1));
       if (k == 0) trace_point(a, r, 2, gt == 0);
     }
   } else {  // R: each stage of every rank's buffer -> rank-order sum -> .grad
-    const int gt = threadIdx.x - kPackThreads;
+    const int gt = threadIdx.x - np;
 #pragma unroll 1
     for (int k = 0; k < K; ++k) {
-      group_wait<W>(a, r, 0, a.seq + (uint32_t)(k + 1), 2, gt, kReadThreads, &packed, (uint32_t)(k + 1));
+      group_wait<W>(a, r, 0, a.seq + (uint32_t)(k + 1), 2, gt, nr, &packed, (uint32_t)(k + 1));
       if (k == 0) trace_point(a, r, 3, gt == 0);
       int64_t lo, hi;
       stage(k, lo, hi);
-      if (!(a.debug & 1)) grp_sum<T, W, false, MAXS>(sa, lo, hi, buf, nullptr, gstride, gt, kReadThreads);
+      if (!(a.debug & 1)) grp_sum<T, W, false, MAXS>(sa, lo, hi, buf, nullptr, gstride, gt, nr);
       if (k == 0) trace_point(a, r, 4, gt == 0);
     }
     trace_point(a, r, 5, gt == 0);
@@ -248,7 +250,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 0) packed = 0;
   __syncthreads();
   trace_point(a, r, 0, threadIdx.x == 0);
-  if (threadIdx.x < kPackThreads) {  // P: pack + scale stage k of chunk c of every shard, publish (kind 0)
+  const int np = a.pack_threads, nr = kThreads - np;
+  if (threadIdx.x < np) {  // P: pack + scale stage k of chunk c of every shard, publish (kind 0)
     const int gt = threadIdx.x;
 #pragma unroll 1
     for (int k = 0; k < K; ++k) {
@@ -256,34 +259,34 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int j = 0; j < W; ++j) {
         int64_t lo, hi;
         rng((r + 1 + j) % W, k, lo, hi);  // own shard last: the peers need theirs first
-        if (!(a.debug & 2)) grp_pack<T, MAXS>(sa, lo, hi, own, a.scale, gstride, gt, kPackThreads);
+        if (!(a.debug & 2)) grp_pack<T, MAXS, 8>(sa, lo, hi, own, a.scale, gstride, gt, np);
       }
       if (k == 0) trace_point(a, r, 1, gt == 0);
-      group_publish<W>(a, r, 0, a.seq + (uint32_t)(k + 1), 1, gt, kPackThreads, &packed, (uint32_t)(k + 1));
+      group_publish<W>(a, r, 0, a.seq + (uint32_t)(k + 1), 1, gt, np, &packed, (uint32_t)(k + 1));
       if (k == 0) trace_point(a, r, 2, gt == 0);
     }
   } else {
-    const int gt = threadIdx.x - kPackThreads;
+    const int gt = threadIdx.x - np;
 #pragma unroll 1
     for (int k = 0; k <= K; ++k) {
       if (k < K) {  // R: own shard, stage k: sum over the W buffers -> own buffer + .grad; publish (kind 1)
-        group_wait<W>(a, r, 0, a.seq + (uint32_t)(k + 1), 2, gt, kReadThreads, &packed, (uint32_t)(k + 1));
+        group_wait<W>(a, r, 0, a.seq + (uint32_t)(k + 1), 2, gt, nr, &packed, (uint32_t)(k + 1));
         if (k == 0) trace_point(a, r, 3, gt == 0);
         int64_t lo, hi;
         rng(r, k, lo, hi);
-        if (!(a.debug & 1)) grp_sum<T, W, true, MAXS>(sa, lo, hi, buf, own, gstride, gt, kReadThreads);
+        if (!(a.debug & 1)) grp_sum<T, W, true, MAXS>(sa, lo, hi, buf, own, gstride, gt, nr);
         if (k == 0) trace_point(a, r, 4, gt == 0);
-        group_publish<W>(a, r, 1, a.seq + (uint32_t)(k + 1), 2, gt, kReadThreads, nullptr, 0);
+        group_publish<W>(a, r, 1, a.seq + (uint32_t)(k + 1), 2, gt, nr, nullptr, 0);
       }
       if (k >= 1) {  // G: every other shard j, stage k-1, from rank j's buffer (its sums) -> .grad
-        group_wait<W>(a, r, 1, a.seq + (uint32_t)k, 2, gt, kReadThreads, nullptr, 0);
+        group_wait<W>(a, r, 1, a.seq + (uint32_t)k, 2, gt, nr, nullptr, 0);
 #pragma unroll 1
         for (int i = 1; i < W; ++i) {
           const int j = (r + i) % W;
           int64_t lo, hi;
           rng(j, k - 1, lo, hi);
           const T* src[1] = {buf[j]};
-          if (!(a.debug & 1)) grp_sum<T, 1, false, MAXS>(sa, lo, hi, src, nullptr, gstride, gt, kReadThreads);
+          if (!(a.debug & 1)) grp_sum<T, 1, false, MAXS>(sa, lo, hi, src, nullptr, gstride, gt, nr);
         }
       }
     }

@@ -240,6 +240,75 @@ def test_algorithm_selection_and_storage_layout():
         L.ddp_destroy(one)
 
 
+def _algos(ctx):
+    return [L.ALGO_NAMES[L.ddp_bucket_algo(ctx, b)] for b in range(L.ddp_num_buckets(ctx))]
+
+
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_policies_per_world(world):
+    """the default (throughput) policy — W=2: the fused one-shot at
+    every size (pull kernels), CE with the round-1 push kernels; W>2: one-shot up
+    to 1 MiB, two-shot above — and PREFER_OVERLAP=1 (the front end's fp32
+    policy): copy engines for every bucket but the last (CE at W=2, CE2 wider),
+    the fused kernel for the last; PREFER_OVERLAP=2: fused everywhere."""
+    ns = numels("resnet50")
+    fused = "oneshot" if world == 2 else "twoshot"
+    ctx = L.ddp_create(ns, L.FP32, 25 * MIB, world, 0)
+    try:
+        sizes = [L.ddp_bucket_info(ctx, b)[0] * 4 for b in range(L.ddp_num_buckets(ctx))]
+        assert _algos(ctx) == ["oneshot" if world == 2 or s <= MIB else "twoshot" for s in sizes]
+        L.ddp_set_option(ctx, L.OPT_PREFER_OVERLAP, 1)
+        a = _algos(ctx)
+        assert a[:-1] == ["ce" if world == 2 else "ce2"] * (len(a) - 1) and a[-1] == fused
+        L.ddp_set_option(ctx, L.OPT_PREFER_OVERLAP, 2)
+        assert set(_algos(ctx)) == {fused}
+        L.ddp_set_option(ctx, L.OPT_PREFER_OVERLAP, 0)
+        L.ddp_set_option(ctx, L.OPT_P2P_PULL, 0)
+        if world == 2:
+            assert set(_algos(ctx)) == {"ce"}
+    finally:
+        L.ddp_destroy(ctx)
+
+
+def test_pull_kernels_double_buffer_fused_buckets():
+    """Pull kernels (default): every fused bucket gets a second buffer (pass
+    parity) instead of per-lane staging, so the storage grows by exactly the
+    fused buckets' aligned bytes over a layout with neither."""
+    ns = numels("resnet50")
+    sizes = None
+    ctx = L.ddp_create(ns, L.FP32, 25 * MIB, 4, 0)
+    try:
+        L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_NCCL)              # no fused bucket: no second buffers
+        base = L.ddp_storage_bytes(ctx)
+        sizes = [L.ddp_bucket_info(ctx, b)[0] * 4 for b in range(L.ddp_num_buckets(ctx))]
+        L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_TWOSHOT)
+        pull = L.ddp_storage_bytes(ctx)
+        assert pull - base == sum((s + 255) // 256 * 256 for s in sizes)
+        L.ddp_set_option(ctx, L.OPT_P2P_PULL, 0)                    # push: per-lane staging instead
+        assert L.ddp_storage_bytes(ctx) != pull
+    finally:
+        L.ddp_destroy(ctx)
+
+
+def test_peer_emulated_bind_checks_before_any_device_call():
+    """ddp_bind_peer_emulated refuses what it cannot emulate before touching a
+    GPU: world 1, missing storages, buckets that need NCCL (> 1024 slots)."""
+    c1 = L.ddp_create(numels("toy"), L.FP32, 4096, 1, 0)
+    try:
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_bind_peer_emulated(c1, 0, 0, [256])
+        assert e.value.status == L.ERR_INVALID_ARG
+    finally:
+        L.ddp_destroy(c1)
+    big = L.ddp_create([1] * 2000, L.FP32, 1 << 30, 2, 1)           # one bucket of 2000 slots -> NCCL
+    try:
+        with pytest.raises(L.DDPError) as e:
+            L.ddp_bind_peer_emulated(big, 0, 0, [256, 512])
+        assert e.value.status == L.ERR_UNSUPPORTED and "NCCL" in str(e.value)
+    finally:
+        L.ddp_destroy(big)
+
+
 def test_mark_unused_protocol():
     """ddp_mark_unused is a ready signal (Alg. 1 forward L224-L225): buckets
     holding unused params launch without their hooks, in order (O-2 replay of
