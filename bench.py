@@ -61,7 +61,8 @@ def parse():
     ap.add_argument("--high-priority", action="store_true",
                     help="communication streams at the highest priority (default: lowest)")
     ap.add_argument("--lanes", type=int, default=0, help="P2P/NVLS kernel lanes (streams)")
-    ap.add_argument("--p2p-push", action="store_true", help="round-1 push kernels instead of the pull kernels")
+    ap.add_argument("--p2p-push", action="store_true", help="push kernels for every fused bucket (DDP_OPT_P2P_PULL=0)")
+    ap.add_argument("--p2p-pull-all", action="store_true", help="pull kernels for every fused bucket (DDP_OPT_P2P_PULL=2)")
     ap.add_argument("--last-on-lane", action="store_true", help="DDP_OPT_LAST_ON_PRODUCER=0")
     ap.add_argument("--wire-bf16", action="store_true", help="N-3: fp32 gradients travel as bf16 (CE exchange)")
     ap.add_argument("--grad-view", action="store_true",
@@ -243,6 +244,8 @@ def run_ours(a):
         opts[L.OPT_LANES] = a.lanes
     if a.p2p_push:
         opts[L.OPT_P2P_PULL] = 0
+    if a.p2p_pull_all:
+        opts[L.OPT_P2P_PULL] = 2
     if a.last_on_lane:
         opts[L.OPT_LAST_ON_PRODUCER] = 0
     if a.wire_bf16:
@@ -900,6 +903,8 @@ def _opts(a):
         o[L.OPT_LANES] = a.lanes
     if a.p2p_push:
         o[L.OPT_P2P_PULL] = 0
+    if a.p2p_pull_all:
+        o[L.OPT_P2P_PULL] = 2
     if a.last_on_lane:
         o[L.OPT_LAST_ON_PRODUCER] = 0
     if a.wire_bf16:

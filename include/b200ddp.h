@@ -148,12 +148,17 @@ enum {
   DDP_OPT_EMU_DEAD_RANK = 22,   /* test support, cooperative emulation only (ddp_bind_emulated):
                                    this rank's CTAs return at once and never signal, so the others
                                    must time out (DDP_OPT_P2P_TIMEOUT_MS).  -1 (default) = none */
-  DDP_OPT_P2P_PULL = 23,        /* fused ONESHOT / TWOSHOT kernels at world > 1: 1 (default) pull
-                                   form — each rank packs into its own bucket buffer (two per bucket,
-                                   alternating by pass) and reads its peers' buffers; the release
-                                   before each flag drains local stores only, .grad is written by
-                                   the reads (no unpack pass, no closing barrier).  0: push form
-                                   (remote stores into per-lane staging, round 1).  Layout key */
+  DDP_OPT_P2P_PULL = 23,        /* which fused ONESHOT / TWOSHOT buckets (world > 1) run the pull form
+                                   (kernels/pull.cu): each rank packs into its own bucket buffer (two
+                                   per bucket, alternating by pass) and reads its peers' buffers; the
+                                   release before each flag drains local stores only and .grad is
+                                   written by the reads (no unpack pass, no closing barrier).  The
+                                   others run the push form (remote stores into per-lane staging,
+                                   round 1), whose stores need ~3x fewer SMs for the same NVLink rate.
+                                   1 (default): pull for the LAST bucket (every SM) and, at world 2
+                                   under the throughput policy (PREFER_OVERLAP 0), for every bucket;
+                                   push for the buckets that run beside backward on COMM_CTAS CTAs;
+                                   2: pull for every fused bucket; 0: push everywhere.  Layout key */
   DDP_OPT_P2P_SIGNAL = 24,      /* pull kernels: how a group publishes "my (local) stores are done"
                                    after its named barrier.  0 (default): fence.acq_rel.gpu +
                                    st.relaxed.sys of the flag into each peer (reading A-1);

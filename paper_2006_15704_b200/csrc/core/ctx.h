@@ -46,6 +46,7 @@ struct Bucket {
   int64_t byte_off = 0;         // inside the symmetric storage
   int64_t alt_off = 0;          // pull kernels: second buffer (pass parity), inside the storage
   uint32_t p2p_count = 0;       // fused launches of this bucket so far (pass parity)
+  bool pull = false;            // fused bucket run by the pull kernels (kernels/pull.cu)
   int algo = DDP_ALGO_NCCL;
   int ctas = 1;
   int64_t shard = 0, chunk = 0, sub = 0;
@@ -103,7 +104,7 @@ struct ddp_ctx {
   int64_t p2p_timeout_ms = 30000;   // bound of every P2P / NVLS barrier spin (%globaltimer)
   int64_t wait_timeout_ms = 60000;  // peer emulation: bound of a host wait for a peer's issue
   int64_t emu_dead_rank = -1;       // test support (cooperative emulation): this rank never signals
-  int64_t p2p_pull = 1;             // fused P2P kernels: 1 pull (kernels/pull.cu), 0 push (kernels/p2p.cu)
+  int64_t p2p_pull = 1;             // fused kernels: 0 push everywhere, 1 pull for the last bucket, 2 pull everywhere
   int64_t p2p_signal = 0;           // pull kernels: flag publication mode (DDP_OPT_P2P_SIGNAL)
   int64_t p2p_debug = 0;            // measurement only: skip data phases (DDP_OPT_P2P_DEBUG)
   int64_t last_on_producer = 1;     // the pass's last fused bucket runs on its producer stream

@@ -418,7 +418,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   for (int r = 0; r < c->world; ++r) a.storage[r] = c->storage[r];
   a.flags_byte_off = c->flags_off + ln * kFlagsBytes;
   a.bucket_byte_off = bk.byte_off;
-  a.pull = c->p2p_pull && c->world > 1 && bk.algo != DDP_ALGO_NVLS ? 1 : 0;
+  a.pull = bk.pull ? 1 : 0;
   if (a.pull) {  // this pass's buffer of the bucket (pass parity, identical on every rank)
     a.bucket_byte_off = (bk.p2p_count++ & 1) ? bk.alt_off : bk.byte_off;
     a.stage_byte_off = 0;

@@ -145,8 +145,11 @@ void grid_for(const ddp_ctx* c, Bucket& bk, int max_ctas) {
   bk.ctas = (int)C;
   // pipeline stage: DDP_OPT_P2P_STAGE_BYTES, else (pull kernels: the pack warps run
   // ahead of the read warps stage by stage) kPullStageBytes, else the whole chunk
-  const bool pull = c->p2p_pull && c->world > 1 && bk.algo != DDP_ALGO_NVLS;
-  const int64_t stage = c->stage_bytes > 0 ? c->stage_bytes : pull ? kPullStageBytes : 0;
+  const bool pull = bk.pull;
+  // (the two-shot packs a stage of EVERY shard before publishing it: W x the stage)
+  const int64_t pull_stage = bk.algo == DDP_ALGO_TWOSHOT
+                                 ? std::max<int64_t>(8 << 10, 2 * kPullStageBytes / c->world) : kPullStageBytes;
+  const int64_t stage = c->stage_bytes > 0 ? c->stage_bytes : pull ? pull_stage : 0;
   bk.sub = stage > 0 ? std::max<int64_t>(kAlignElems, std::min<int64_t>(Q, stage / c->esize)) : Q;
   bk.stages = (int32_t)cdiv(Q, bk.sub);
 }
@@ -160,7 +163,7 @@ int max_ctas_for(const ddp_ctx* c, const Bucket& bk) {
   if (c->emulated || c->peer_emu) {
     // every rank of a launch in one cooperative kernel; in peer emulation the
     // lanes' kernels must also fit side by side (they spin independently)
-    const int e = emulated_max_ctas(bk.algo, c->dtype, (int)bk.params.size(), c->world, c->p2p_pull != 0);
+    const int e = emulated_max_ctas(bk.algo, c->dtype, (int)bk.params.size(), c->world, bk.pull);
     m = std::min(m, std::max(1, e / (c->peer_emu ? lanes_in_use(c) : 1)));
   }
   return std::max(1, m);
@@ -175,7 +178,19 @@ void plan(ddp_ctx* c) {
     bk.algo = resolve_algo(c, bk);
     bk.byte_off = pos;
     pos += align_up(bk.numel * c->esize, 256);
-    if (c->p2p_pull && c->world > 1) continue;  // pull kernels: no staging (second buffer below)
+    // which fused buckets run the pull kernels (DDP_OPT_P2P_PULL): they read the
+    // peers' buffers, so a CTA's remote throughput is bounded by loads in flight
+    // (~5-8 GB/s per SM measured) — best with every SM, i.e. for the LAST bucket;
+    // the push kernels' fire-and-forget stores are ~3x more SM-efficient, so the
+    // buckets that run beside backward on COMM_CTAS CTAs keep them.  Exception
+    // (measured, profiles/r02_pull.md): with every bucket ready at once at W=2 (the
+    // throughput policy) the lanes' pull one-shots together saturate the links and
+    // beat both the push one-shot and the copy engines on the step
+    bk.pull = c->world > 1 && (bk.algo == DDP_ALGO_ONESHOT || bk.algo == DDP_ALGO_TWOSHOT) &&
+              (c->p2p_pull == 2 ||
+               (c->p2p_pull == 1 &&
+                (&bk == &c->buckets.back() || (c->world == 2 && c->prefer_overlap == 0))));
+    if (bk.pull) continue;  // pull kernels: no staging (second buffer below)
     if (bk.algo == DDP_ALGO_TWOSHOT) l2max = std::max(l2max, align_up(cdiv(bk.numel, c->world), kAlignElems));
     if (bk.algo == DDP_ALGO_ONESHOT && c->world > 1) n1max = std::max(n1max, align_up(bk.numel, kAlignElems));
   }
@@ -188,7 +203,7 @@ void plan(ddp_ctx* c) {
   // pull kernels: a second buffer per fused bucket; pass v uses buffer v % 2 (kernels/pull.cu)
   for (Bucket& bk : c->buckets) {
     bk.alt_off = bk.byte_off;
-    if (c->p2p_pull && c->world > 1 && (bk.algo == DDP_ALGO_ONESHOT || bk.algo == DDP_ALGO_TWOSHOT)) {
+    if (bk.pull) {
       bk.alt_off = pos;
       pos += align_up(bk.numel * c->esize, 256);
     }
@@ -930,7 +945,8 @@ ddp_status_t ddp_set_option(ddp_ctx_t* c, int32_t key, int64_t v) {
       c->wait_timeout_ms = v;
       return DDP_OK;
     case DDP_OPT_P2P_PULL:
-      c->p2p_pull = v ? 1 : 0;
+      if (v < 0 || v > 2) return fail(DDP_ERR_INVALID_ARG, "P2P_PULL must be 0, 1 or 2");
+      c->p2p_pull = v;
       break;
     case DDP_OPT_P2P_SIGNAL:
       if (v < 0 || v > 3) return fail(DDP_ERR_INVALID_ARG, "P2P_SIGNAL must be 0..3");

@@ -271,21 +271,24 @@ def test_policies_per_world(world):
 
 
 def test_pull_kernels_double_buffer_fused_buckets():
-    """Pull kernels (default): every fused bucket gets a second buffer (pass
-    parity) instead of per-lane staging, so the storage grows by exactly the
-    fused buckets' aligned bytes over a layout with neither."""
+    """Pull kernels: a fused bucket run by them gets a second buffer (pass
+    parity) instead of per-lane staging.  P2P_PULL=2: every fused bucket;
+    1 (default): only the last one, the others keep the push form's per-lane
+    two-shot staging (LANES x W slots of the largest shard)."""
     ns = numels("resnet50")
-    sizes = None
-    ctx = L.ddp_create(ns, L.FP32, 25 * MIB, 4, 0)
+    W, lanes = 4, 4
+    ctx = L.ddp_create(ns, L.FP32, 25 * MIB, W, 0)
     try:
         L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_NCCL)              # no fused bucket: no second buffers
         base = L.ddp_storage_bytes(ctx)
         sizes = [L.ddp_bucket_info(ctx, b)[0] * 4 for b in range(L.ddp_num_buckets(ctx))]
+        a256 = lambda x: (x + 255) // 256 * 256
         L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_TWOSHOT)
-        pull = L.ddp_storage_bytes(ctx)
-        assert pull - base == sum((s + 255) // 256 * 256 for s in sizes)
-        L.ddp_set_option(ctx, L.OPT_P2P_PULL, 0)                    # push: per-lane staging instead
-        assert L.ddp_storage_bytes(ctx) != pull
+        L.ddp_set_option(ctx, L.OPT_P2P_PULL, 2)
+        assert L.ddp_storage_bytes(ctx) - base == sum(a256(s) for s in sizes)
+        L.ddp_set_option(ctx, L.OPT_P2P_PULL, 1)
+        shard = max(((s // 4 + W - 1) // W + 255) // 256 * 256 for s in sizes[:-1])
+        assert L.ddp_storage_bytes(ctx) - base == a256(sizes[-1]) + lanes * W * a256(shard * 4)
     finally:
         L.ddp_destroy(ctx)
 

@@ -250,11 +250,12 @@ def test_bert_large_emulated_sampled(W, dtype):
 @pytest.mark.parametrize("W", [2, 3, 4])
 @pytest.mark.parametrize("algo", [L.ALGO_ONESHOT, L.ALGO_TWOSHOT])
 def test_pull_and_push_kernels_every_signal_mode(W, algo):
-    """The fused kernels in both forms (pull, the default, and the round-1 push),
+    """The fused kernels in both forms (pull, push, and the default mix: pull for the last bucket),
     every flag-publication mode of the pull form and pipelined stages: bit-exact
     vs O-3b over 3 passes (the pull form alternates two buffers per bucket)."""
     ns = numels("resnet50")[:50]
-    for opts in ([{L.OPT_P2P_PULL: 0}, {L.OPT_P2P_PULL: 0, L.OPT_P2P_STAGE_BYTES: 16 << 10}]
-                 + [{L.OPT_P2P_SIGNAL: m, L.OPT_P2P_STAGE_BYTES: st} for m in range(4) for st in (0, 16 << 10)]):
+    for opts in ([{L.OPT_P2P_PULL: 0}, {L.OPT_P2P_PULL: 0, L.OPT_P2P_STAGE_BYTES: 16 << 10}, {L.OPT_P2P_PULL: 1}]
+                 + [{L.OPT_P2P_PULL: 2, L.OPT_P2P_SIGNAL: m, L.OPT_P2P_STAGE_BYTES: st}
+                    for m in range(4) for st in (0, 16 << 10)]):
         ins, outs, offs = run_emulated(ns, "fp32", 2 * MIB, W, algo, iters=3, misalign=True, options=opts)
         _check_bitfaithful(ins, outs, offs, ns, "fp32", W)

@@ -91,6 +91,9 @@ RESNET = [  # (W, algo, options, dtype): the shipped policies and every forced e
     (8, L.ALGO_AUTO, {}, "fp32"),
     (8, L.ALGO_AUTO, {L.OPT_PREFER_OVERLAP: 1}, "fp32"),
     (8, L.ALGO_CE, {}, "bf16"),
+    (4, L.ALGO_AUTO, {L.OPT_P2P_PULL: 2}, "fp32"),                  # pull kernels for every bucket
+    (2, L.ALGO_AUTO, {L.OPT_P2P_PULL: 0}, "bf16"),                  # push kernels only (round 1)
+    (8, L.ALGO_TWOSHOT, {L.OPT_P2P_PULL: 2}, "bf16"),
 ]
 
 
