@@ -172,6 +172,8 @@ struct ddp_ctx {
   cudaStream_t producer = nullptr;     // stream of the most recent ready signal
   bool from_signal = false;            // device work issued from a ready signal (not finalize)
   cudaStream_t last_on = nullptr;      // the pass's last bucket ran on this producer stream
+  cudaStream_t done_stream = nullptr;  // stream comm_done was last recorded on
+  bool lone_last = false;              // this pass's only device work: the last bucket on its producer
   std::vector<cudaEvent_t> join_ev;    // joins of library streams into last_on
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> stream_events;
   cudaEvent_t comm_done = nullptr;

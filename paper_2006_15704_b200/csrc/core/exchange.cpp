@@ -388,6 +388,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   // joined into it: the pass then ends on the producer stream, and the two
   // cross-stream hops (producer -> comm, comm -> producer) of its sync disappear.
   const bool on_producer = last && c->last_on_producer && c->from_signal && c->producer && !c->find_unused;
+  if (c->lone_last && !on_producer) return fail(DDP_ERR_STATE, "internal: lone last bucket off its producer");
   auto join = [&](cudaStream_t q, cudaStream_t into, size_t& k) -> ddp_status_t {
     if (!q || q == into) return DDP_OK;
     if (k >= c->join_ev.size()) return fail(DDP_ERR_STATE, "join event pool exhausted");
@@ -396,14 +397,14 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
     return DDP_OK;
   };
   size_t nj = 0;
-  if (last) {
+  if (on_producer) ls = c->producer;
+  if (last && !c->lone_last) {
     // The last bucket's kernel uses every SM (max_ctas_for) and spins until the
     // peers arrive.  Everything this rank launched before it must be finished
     // first: the other lanes' spinning kernels (so all of its CTAs can be
     // resident), and the copy-engine paths' kernels of earlier buckets (else
     // they would wait for SMs behind a kernel that waits for peers — measured
     // as a 0.8 ms stall at W=4, profiles/r01_n4.md).
-    if (on_producer) ls = c->producer;
     for (int k = 0; k < nl; ++k) {
       cudaStream_t ks = k == 0 ? c->comm : c->lane_stream[k];
       if (ks == ls && !on_producer) continue;
@@ -463,7 +464,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
     CUDA_TRY(c, launch_p2p(bk.algo, c->dtype, sv, a, ls));
   }
   prof_end(c, ls);
-  if (on_producer) {  // the copy-only streams join after the kernel (they hold no SMs)
+  if (on_producer && !c->lone_last) {  // the copy-only streams join after the kernel (they hold no SMs)
     for (cudaStream_t ks : {c->ce_ag})
       if (ddp_status_t st = join(ks, ls, nj)) return st;
     for (cudaStream_t ks : c->ce2_rs)
@@ -472,8 +473,8 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
       if (ddp_status_t st = join(ks, ls, nj)) return st;
     for (size_t k = 1; k < c->rr_stream.size(); ++k)
       if (ddp_status_t st = join(c->rr_stream[k], ls, nj)) return st;
-    c->last_on = ls;
   }
+  if (on_producer) c->last_on = ls;
   return DDP_OK;
 }
 
@@ -510,6 +511,21 @@ ddp_status_t device_range(ddp_ctx* c, int b0, int b1) {
     cudaEvent_t ev = pool_event(c);
     CUDA_TRY(c, cudaEventRecord(ev, c->unwaited.empty() ? c->comm : c->unwaited.front()));
     c->prof_ready.push_back(ev);
+  }
+  // A pass whose first device work is the last bucket alone (a one-bucket model,
+  // or every other bucket synced earlier... i.e. nothing else launched) runs that
+  // bucket on its producer stream with no cross-stream hop at all (launch_device):
+  // the producer only has to follow the previous pass's end.
+  const Bucket& lb = c->buckets.back();
+  c->lone_last = !c->pass_launched && b0 == (int)c->buckets.size() - 1 && b1 == (int)c->buckets.size() &&
+                 c->world > 1 && !c->emulated && c->last_on_producer && c->from_signal && c->producer &&
+                 !c->find_unused &&
+                 (lb.algo == DDP_ALGO_ONESHOT || lb.algo == DDP_ALGO_TWOSHOT || lb.algo == DDP_ALGO_NVLS);
+  if (c->lone_last) {
+    c->pass_launched = true;
+    c->unwaited.clear();
+    if (c->comm_done_valid && c->done_stream != c->producer)
+      CUDA_TRY(c, cudaStreamWaitEvent(c->producer, c->comm_done, 0));
   }
   // comm stream waits for everything the producers enqueued so far
   for (cudaStream_t s : c->unwaited) {

@@ -300,6 +300,7 @@ void open_pass(ddp_ctx* c) {
   c->state = State::IN_PASS;
   c->pass_launched = false;
   c->last_on = nullptr;
+  c->lone_last = false;
   c->pass_no_sync = c->no_sync;  // reading C-9
   std::fill(c->ready.begin(), c->ready.end(), 0);
   for (size_t b = 0; b < c->buckets.size(); ++b) c->pending[b] = (int32_t)c->buckets[b].params.size();
@@ -746,7 +747,9 @@ ddp_status_t ddp_grads_ready(ddp_ctx_t* c, int32_t n, const int32_t* params, voi
   // buckets completed by the batch are launched even if a later signal failed:
   // their launch is already part of the (cross-rank) launch sequence
   const std::string err = g_err;
+  c->from_signal = true;  // the batch's buckets were completed by its ready signals
   ddp_status_t st2 = device_range(c, c->defer_b0, c->defer_b1);
+  c->from_signal = false;
   if (st != DDP_OK) {
     g_err = err;
     return st;
@@ -829,6 +832,7 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
       cudaStream_t end = c->last_on ? c->last_on : c->comm;
       CUDA_TRY(c, cudaEventRecord(c->comm_done, end));
       c->comm_done_valid = true;
+      c->done_stream = end;
       if (static_cast<cudaStream_t>(consumer_stream) != end)
         CUDA_TRY(c, cudaStreamWaitEvent(static_cast<cudaStream_t>(consumer_stream), c->comm_done, 0));
       c->ce_used = c->ce2_used = false;

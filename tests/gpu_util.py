@@ -182,15 +182,25 @@ class PeerEmu:
         torch.cuda.synchronize()
         return out.cpu()
 
-    def sync_pass(self, orders=None, unused=None, no_sync=False):
+    def sync_pass(self, orders=None, unused=None, no_sync=False, late_fill=None):
         """One backward pass on every rank's thread: ready signals in orders[r]
         (default reverse registration), unused[r] = params marked unused
-        (ddp_mark_unused with the current gradient buffer), then finalize."""
+        (ddp_mark_unused with the current gradient buffer), then finalize.
+        late_fill = (seed, it, dist): each rank's thread first stalls its producer
+        stream (~2 ms GPU sleep) and only then generates its gradients ON that
+        stream, right before the ready signals — the library must order its device
+        work after the producer stream, or it reads stale gradients."""
         torch.cuda.synchronize()
         n = len(self.ns)
 
         def rank(r):
             c, s = self.ctx[r], self.prod[r].cuda_stream
+            if late_fill is not None:
+                seed, it, dist = late_fill
+                with torch.cuda.stream(self.prod[r]):
+                    torch.cuda._sleep(4_000_000)
+                for p, g in enumerate(self.grads[r]):
+                    sdev.fill(g, seed, r, it, p, dist, self.dtype, s)
             if no_sync:
                 L.ddp_no_sync_begin(c)
             un = set((unused or {}).get(r, ()))

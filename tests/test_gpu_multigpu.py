@@ -126,7 +126,10 @@ def test_multigpu_parity(world):
             # gradient-as-bucket-view (N-3): CE in place at W=2, CE2 wider (bit-exact); NCCL when forced
             ("resnet50", "fp32", 25 * MIB, L.ALGO_AUTO, 2, {L.OPT_GRAD_VIEW: 1}),
             ("bert_large", "bf16", 25 * MIB, L.ALGO_AUTO, 1, {L.OPT_GRAD_VIEW: 1}),
-            ("toy", "fp32", 4096, L.ALGO_NCCL, 2, {L.OPT_GRAD_VIEW: 1})]
+            ("toy", "fp32", 4096, L.ALGO_NCCL, 2, {L.OPT_GRAD_VIEW: 1}),
+            ("resnet50", "fp32", 1 << 30, L.ALGO_AUTO, 3),          # one bucket: the lone-last-bucket pass
+            ("resnet50", "bf16", 25 * MIB, L.ALGO_AUTO, 2, {L.OPT_P2P_PULL: 2}),
+            ("resnet50", "fp32", 25 * MIB, L.ALGO_AUTO, 2, {L.OPT_PREFER_OVERLAP: 2})]
     outs = _run(world, cfgs)
     for ci, cfg in enumerate(cfgs):
         model, dtype, cap, algo, iters = cfg[:5]

@@ -105,6 +105,41 @@ def test_resnet50_full(W, algo, opts, dtype):
     _check(ins, outs, offs, ns, dtype, W)
 
 
+@pytest.mark.parametrize("W", [2, 4])
+def test_single_bucket_passes(W):
+    """A model in ONE bucket: every pass's only device work is the last bucket,
+    run on its producer stream with no cross-stream hop (exchange.cpp lone_last);
+    three passes alternate the pull buffers and follow each other only through
+    the producer stream."""
+    ns = numels("resnet50")
+    ins, outs, offs = run_peer_emulated(ns, "fp32", 1 << 30, W, L.ALGO_AUTO, iters=3)
+    _check(ins, outs, offs, ns, "fp32", W)
+
+
+@pytest.mark.parametrize("W,cap,algo", [(2, 1 << 30, L.ALGO_AUTO), (4, 1 << 30, L.ALGO_AUTO),
+                                         (2, 4096, L.ALGO_AUTO), (4, 4096, L.ALGO_AUTO),
+                                         (2, 4096, L.ALGO_CE), (4, 4096, L.ALGO_CE2), (3, 4096, L.ALGO_PUSH)])
+def test_device_work_follows_the_producer_stream(W, cap, algo):
+    """P:L184-L186 / a5: every bucket's device work is ordered after the hooks'
+    producer stream.  Each rank stalls its producer stream, generates its
+    gradients on it and only then signals: any launch not ordered after the
+    producer would read the previous pass's gradients and miss O-3b."""
+    ns = numels("toy")
+    pe = PeerEmu(ns, "fp32", cap, W, algo)
+    try:
+        for it in range(3):
+            pe.sync_pass(late_fill=(77, it, "normal"))
+            out = param_slices(pe.snapshot(), pe.offs, ns, "fp32")
+            for p, n in enumerate(ns):
+                want = average_bitfaithful([gen_values(77, r, it, p, np.arange(n), "normal", "fp32")
+                                            for r in range(W)], "fp32")
+                for r in range(W):
+                    assert np.array_equal(out[r][p], want), (it, p, r)
+        pe.check_guards()
+    finally:
+        pe.close()
+
+
 def test_knobs_never_change_values():
     """cap, exchange, streams and CTA counts change time, never bits."""
     ns = numels("resnet50")[:60]
