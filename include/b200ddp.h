@@ -124,21 +124,22 @@ enum {
   DDP_OPT_GRAD_VIEW = 19,       /* gradient-as-bucket-view (§8(f) N-3, zero-copy variant; the
                                    paper's buckets hold copies, Alg. 1 L231-L232 / L246): 1 = the
                                    caller places each gradient AT its bucket slot in this rank's
-                                   storage (ddp_param_storage_offset), so a3 and a6 vanish.  Every
-                                   bucket uses DDP_ALGO_CE at world 2 (the bucket region travels as
-                                   one copy-engine transfer per peer, the rank-order reduce writes
-                                   back in place) and DDP_ALGO_CE2 wider (reduce-scatter copies of
-                                   the raw region, each operand x fl(1/W) in the shard reduce,
-                                   all-gather into the peers' regions): O-3b, bit-exact.  With
-                                   DDP_OPT_ALGO = NCCL, or at world 1: an in-place ncclAllReduce with
-                                   ncclAvg (each operand x fl(1/W), then the sum — O-3b up to NCCL's
-                                   summation order).  A gradient passed at any other
-                                   address is still correct: it is copied raw into its slot before
-                                   and back after the allreduce.  Not combinable with FIND_UNUSED
-                                   or WIRE_BF16 (DDP_ERR_UNSUPPORTED).  At world > 2 every bucket
-                                   then uses CE2, including the last one (no fused two-shot on
-                                   every SM): measured slower than the default policy at W=4
-                                   (profiles/r01_grad_view.md).  Default 0; layout key */
+                                   storage (ddp_param_storage_offset), so a3 and a6 vanish and every
+                                   bucket is averaged in place: by the fused two-shot in place
+                                   (kernels/pull.cu pull_view_twoshot_kernel: each rank reads its
+                                   peers' raw gradients, scales every operand by fl(1/W), sums its
+                                   own shard in rank order in place, then reads the peers' sums;
+                                   O-3b, bit-exact), except beside a running backward under
+                                   PREFER_OVERLAP=1, where the copy-engine exchanges run in place (CE
+                                   at world 2: the region as one transfer per peer; CE2 wider).
+                                   DDP_OPT_ALGO = CE / CE2 force those; NCCL (or world 1): an
+                                   in-place ncclAllReduce with ncclAvg (each operand x fl(1/W), then
+                                   the sum — O-3b up to NCCL's summation order).  A gradient passed
+                                   at any other address is still correct: it is copied raw into its
+                                   slot before and back after the exchange.  Not combinable with
+                                   FIND_UNUSED or WIRE_BF16 (DDP_ERR_UNSUPPORTED), nor with
+                                   ddp_bind_emulated (use ddp_bind_peer_emulated).  Default 0; layout
+                                   key */
   DDP_OPT_P2P_TIMEOUT_MS = 20,  /* bound of every barrier spin inside the fused P2P / NVLS kernels
                                    (%globaltimer); a peer that never arrives makes the waiting CTAs
                                    give up, set the error word and exit -> DDP_ERR_TIMEOUT from

@@ -182,7 +182,7 @@ static ddp_status_t launch_all(ddp_ctx* c, EmuGroup* g, EmuRdv& R, int lane, std
     bool same = d.algo == d0.algo && d.sv.n == d0.sv.n && d.a.numel == d0.a.numel && d.a.ctas == d0.a.ctas &&
                 d.a.seq == d0.a.seq && d.a.stage_byte_off == d0.a.stage_byte_off &&
                 d.a.bucket_byte_off == d0.a.bucket_byte_off;
-    for (int k = 0; same && k < d.sv.n; ++k)
+    for (int k = 0; same && !d.a.view && k < d.sv.n; ++k)  // the in-place form uses no slot table
       same = (const char*)d.sv.grad[k] - (const char*)d0.sv.grad[k] == (int64_t)r * stride &&
              d.sv.off[k] == d0.sv.off[k];
     if (!same) {

@@ -420,7 +420,11 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   a.flags_byte_off = c->flags_off + ln * kFlagsBytes;
   a.bucket_byte_off = bk.byte_off;
   a.pull = bk.pull ? 1 : 0;
-  if (a.pull) {  // this pass's buffer of the bucket (pass parity, identical on every rank)
+  a.view = c->grad_view && bk.algo == DDP_ALGO_TWOSHOT && c->world > 1 ? 1 : 0;
+  if (a.view) {  // in place on the gradients (they are the bucket region)
+    a.stage_byte_off = 0;
+    a.stage_stride = 0;
+  } else if (a.pull) {  // this pass's buffer of the bucket (pass parity, identical on every rank)
     a.bucket_byte_off = (bk.p2p_count++ & 1) ? bk.alt_off : bk.byte_off;
     a.stage_byte_off = 0;
     a.stage_stride = 0;
@@ -455,6 +459,10 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
   a.debug = (int32_t)c->p2p_debug;
   c->p2p_seq[ln] += (uint32_t)bk.stages + 2;  // flag values used: seq .. seq + stages + 1
   c->p2p_launches[ln] += 1;
+  // gradient-as-bucket-view: gradients handed over elsewhere are copied raw into
+  // their slots first and back after (on the launching stream, in order)
+  const auto runs = a.view ? alias_runs(c, bk, mine + bk.byte_off) : std::vector<std::pair<int, int>>();
+  if (ddp_status_t st = copy_runs(c, bk, runs, mine + bk.byte_off, true, ls)) return st;
   prof_begin(c, 3, ls);
   if (c->peer_emu) {  // the ranks meet on the host; one cooperative kernel runs them all
     if (ddp_status_t st = emu_p2p_launch(c, bk.algo, sv, a, ls, ln)) return st;
@@ -464,6 +472,7 @@ ddp_status_t launch_device(ddp_ctx* c, int b) {
     CUDA_TRY(c, launch_p2p(bk.algo, c->dtype, sv, a, ls));
   }
   prof_end(c, ls);
+  if (ddp_status_t st = copy_runs(c, bk, runs, mine + bk.byte_off, false, ls)) return st;
   if (on_producer && !c->lone_last) {  // the copy-only streams join after the kernel (they hold no SMs)
     for (cudaStream_t ks : {c->ce_ag})
       if (ddp_status_t st = join(ks, ls, nj)) return st;

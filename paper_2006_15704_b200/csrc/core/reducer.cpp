@@ -84,7 +84,11 @@ int resolve_algo(const ddp_ctx* c, const Bucket& bk) {
   if (c->grad_view) {
     if (c->world == 1 || c->algo == DDP_ALGO_NCCL) return DDP_ALGO_NCCL;
     if (c->algo == DDP_ALGO_CE || c->algo == DDP_ALGO_CE2) return (int)c->algo;
-    return c->world == 2 ? DDP_ALGO_CE : DDP_ALGO_CE2;
+    // beside a running backward (fp32 overlap policy): the SM-free copy engines;
+    // otherwise, and for the last bucket, the fused two-shot in place
+    // (kernels/pull.cu pull_view_twoshot_kernel: no pack, no copy back)
+    if (c->prefer_overlap == 1 && &bk != &c->buckets.back()) return c->world == 2 ? DDP_ALGO_CE : DDP_ALGO_CE2;
+    return (int)bk.params.size() > kMaxSlotsPerLaunch ? DDP_ALGO_NCCL : DDP_ALGO_TWOSHOT;
   }
   int a;
   if (c->algo != DDP_ALGO_AUTO) {
@@ -145,7 +149,7 @@ void grid_for(const ddp_ctx* c, Bucket& bk, int max_ctas) {
   bk.ctas = (int)C;
   // pipeline stage: DDP_OPT_P2P_STAGE_BYTES, else (pull kernels: the pack warps run
   // ahead of the read warps stage by stage) kPullStageBytes, else the whole chunk
-  const bool pull = bk.pull;
+  const bool pull = bk.pull || (c->grad_view && bk.algo == DDP_ALGO_TWOSHOT);
   // (the two-shot packs a stage of EVERY shard before publishing it: W x the stage)
   const int64_t pull_stage = bk.algo == DDP_ALGO_TWOSHOT
                                  ? std::max<int64_t>(8 << 10, 2 * kPullStageBytes / c->world) : kPullStageBytes;
@@ -163,7 +167,8 @@ int max_ctas_for(const ddp_ctx* c, const Bucket& bk) {
   if (c->emulated || c->peer_emu) {
     // every rank of a launch in one cooperative kernel; in peer emulation the
     // lanes' kernels must also fit side by side (they spin independently)
-    const int e = emulated_max_ctas(bk.algo, c->dtype, (int)bk.params.size(), c->world, bk.pull);
+    const int e = emulated_max_ctas(bk.algo, c->dtype, (int)bk.params.size(), c->world, bk.pull,
+                                    c->grad_view && bk.algo == DDP_ALGO_TWOSHOT);
     m = std::min(m, std::max(1, e / (c->peer_emu ? lanes_in_use(c) : 1)));
   }
   return std::max(1, m);
@@ -186,11 +191,11 @@ void plan(ddp_ctx* c) {
     // (measured, profiles/r02_pull.md): with every bucket ready at once at W=2 (the
     // throughput policy) the lanes' pull one-shots together saturate the links and
     // beat both the push one-shot and the copy engines on the step
-    bk.pull = c->world > 1 && (bk.algo == DDP_ALGO_ONESHOT || bk.algo == DDP_ALGO_TWOSHOT) &&
+    bk.pull = c->world > 1 && !c->grad_view && (bk.algo == DDP_ALGO_ONESHOT || bk.algo == DDP_ALGO_TWOSHOT) &&
               (c->p2p_pull == 2 ||
                (c->p2p_pull == 1 &&
                 (&bk == &c->buckets.back() || (c->world == 2 && c->prefer_overlap == 0))));
-    if (bk.pull) continue;  // pull kernels: no staging (second buffer below)
+    if (bk.pull || c->grad_view) continue;  // pull kernels: no staging (second buffer below); view: in place
     if (bk.algo == DDP_ALGO_TWOSHOT) l2max = std::max(l2max, align_up(cdiv(bk.numel, c->world), kAlignElems));
     if (bk.algo == DDP_ALGO_ONESHOT && c->world > 1) n1max = std::max(n1max, align_up(bk.numel, kAlignElems));
   }
@@ -685,6 +690,7 @@ ddp_status_t ddp_bind_emulated(ddp_ctx_t* c, int32_t device, void* comm_stream, 
       return fail(DDP_ERR_UNSUPPORTED, "cooperative emulation runs the one-shot / two-shot kernels only (set "
                                        "DDP_OPT_ALGO, or use ddp_bind_peer_emulated)");
   if (c->find_unused) return fail(DDP_ERR_UNSUPPORTED, "find_unused needs a real communicator (no emulation)");
+  if (c->grad_view) return fail(DDP_ERR_UNSUPPORTED, "gradient-as-bucket-view needs one context per rank (ddp_bind_peer_emulated)");
   if (c->multicast) return fail(DDP_ERR_UNSUPPORTED, "NVLS needs real multicast memory (no emulation)");
   if (ddp_status_t st = bind_common(c, device, comm_stream)) return st;
   for (int r = 0; r < c->world; ++r) c->storage[r] = storages[r];

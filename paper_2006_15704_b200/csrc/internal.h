@@ -49,6 +49,7 @@ struct P2PLaunch {
   int32_t sig_mode;           // pull kernels: how a flag is published (DDP_OPT_P2P_SIGNAL)
   int32_t debug;              // measurement only (DDP_OPT_P2P_DEBUG): 1 skip reads, 2 skip pack
   int32_t pack_threads;       // pull kernels: threads of the pack group (multiple of 32, < kThreads)
+  int32_t view;               // pull two-shot in place on the gradients (DDP_OPT_GRAD_VIEW); no slot table
 };
 
 // Several buckets launched together at world 1: slot k covers virtual elements
@@ -71,6 +72,7 @@ cudaError_t launch_p2p(int algo, int dtype, const SlotView& sv, const P2PLaunch&
 // Pull form of the same two algorithms (kernels/pull.cu): ranks read each other's buffers.
 cudaError_t launch_pull(int algo, int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
 int pull_occupancy(int algo, int dtype, int world, int n_slots);
+int pull_view_occupancy(int dtype, int world);
 // NVLS (NVSwitch multicast) two-shot: pack -> multimem.ld_reduce + multimem.st -> unpack.
 cudaError_t launch_nvls(int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s);
 // Copy-engine algorithm, SM part.  A list of gradients with their element
@@ -115,6 +117,6 @@ struct UnusedView {
 cudaError_t launch_unused_fixup(int dtype, const UnusedView& uv, const int32_t* global_used, int max_ctas,
                                 cudaStream_t s);
 // Largest number of CTAs per rank an emulated launch of `world` ranks may use.
-int emulated_max_ctas(int algo, int dtype, int n_slots, int world, bool pull);
+int emulated_max_ctas(int algo, int dtype, int n_slots, int world, bool pull, bool view = false);
 
 }  // namespace b200ddp

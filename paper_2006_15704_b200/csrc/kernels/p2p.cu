@@ -227,15 +227,16 @@ int occupancy(int algo, int world, int n_slots) {
 }  // namespace
 
 cudaError_t launch_p2p(int algo, int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s) {
-  if (a.pull && a.world > 1) return launch_pull(algo, dtype, sv, a, s);
+  if ((a.pull || a.view) && a.world > 1) return launch_pull(algo, dtype, sv, a, s);
   return dtype == 0 ? dispatch<float>(algo, sv, a, s) : dispatch<__nv_bfloat16>(algo, sv, a, s);
 }
 
-int emulated_max_ctas(int algo, int dtype, int n_slots, int world, bool pull) {
+int emulated_max_ctas(int algo, int dtype, int n_slots, int world, bool pull, bool view) {
   int dev = 0, sms = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return 0;
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
-  const int occ = pull && world > 1 ? pull_occupancy(algo, dtype, world, n_slots)
+  const int occ = view && world > 1   ? pull_view_occupancy(dtype, world)
+                  : pull && world > 1 ? pull_occupancy(algo, dtype, world, n_slots)
                   : dtype == 0 ? occupancy<float>(algo, world, n_slots)
                                : occupancy<__nv_bfloat16>(algo, world, n_slots);
   return occ * sms / (world > 0 ? world : 1);

@@ -296,6 +296,93 @@ __global__ void __launch_bounds__(kThreads, 1)
   trace_point(a, r, 6, threadIdx.x == 0);
 }
 
+// Gradient-as-bucket-view form of the two-shot (DDP_OPT_GRAD_VIEW, §8(f) N-3,
+// zero-copy): every rank's gradients ARE its bucket region, so there is no pack
+// and no second buffer, and the average is written in place:
+//   publish kind 0: this rank's (raw) gradients are final — prior work on the
+//      launching stream produced them;
+//   R  own shard r, stage k: RNE( sum_q RNE(g_q(x) * fl(1/W)) ) over the W ranks'
+//      raw gradients (W-1 read over NVLink), written in place into the own shard
+//      (no peer reads the own shard's raw values: in R each rank reads only its
+//      own shard); publish kind 1 (stage k summed);
+//   G  every other shard j, stage k: rank j's sums -> the own region, once rank j
+//      has published kind 1 for the stage, i.e. finished reading this rank's raw
+//      shard j;
+//   kind 2 at the end: this rank has read every peer's sums; wait for every
+//      peer's, so no sum is still being read when the caller's next backward
+//      overwrites the gradients.
+// Arithmetic = oracle O-3b (each operand x fl(1/W), rank-order fp32 sum, one rounding).
+template <typename T, int W>
+__global__ void __launch_bounds__(kThreads, 1) pull_view_twoshot_kernel(const __grid_constant__ P2PLaunch a) {
+  const int r = a.emulated ? (int)blockIdx.y : a.rank;
+  if (a.emulated && r == a.dead_rank) return;
+  const int c = blockIdx.x;
+  const int64_t L = a.shard, N = a.numel, Q = a.chunk, SUB = a.sub;
+  const int K = a.stages;
+  auto rng = [&](int j, int k, int64_t& lo, int64_t& hi) {
+    const int64_t c0 = (int64_t)c * Q, c1 = min(c0 + Q, L);
+    lo = min(j * L + min(c0 + (int64_t)k * SUB, c1), N);
+    hi = min(j * L + min(c0 + (int64_t)(k + 1) * SUB, c1), N);
+  };
+  T* own = at<T>(a.storage[r], a.bucket_byte_off);
+  const T* buf[W];
+#pragma unroll
+  for (int q = 0; q < W; ++q) buf[q] = at<T>(a.storage[q], a.bucket_byte_off);
+  const int gt = threadIdx.x, nt = kThreads;
+  constexpr int UR = W <= 2 ? 4 : W <= 4 ? 3 : W <= 6 ? 2 : 1;
+  group_publish<W>(a, r, 0, a.seq + (uint32_t)K, 0, gt, nt, nullptr, 0);
+  group_wait<W>(a, r, 0, a.seq + (uint32_t)K, 0, gt, nt, nullptr, 0);
+#pragma unroll 1
+  for (int k = 0; k <= K; ++k) {
+    if (k < K) {  // R
+      int64_t lo, hi;
+      rng(r, k, lo, hi);
+      if (lo < hi && !(a.debug & 1)) {
+        T* d[1] = {own + lo};
+        const T* sp[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) sp[q] = buf[q] + lo;
+        grp_xfer<T, W, 1, false, true, true, UR>(d, sp, hi - lo, a.scale, gt, nt);
+      }
+      group_publish<W>(a, r, 1, a.seq + (uint32_t)(k + 1), 0, gt, nt, nullptr, 0);
+    }
+    if (k >= 1) {  // G, stage k-1
+      group_wait<W>(a, r, 1, a.seq + (uint32_t)k, 0, gt, nt, nullptr, 0);
+#pragma unroll 1
+      for (int i = 1; i < W; ++i) {
+        const int j = (r + i) % W;
+        int64_t lo, hi;
+        rng(j, k - 1, lo, hi);
+        if (lo >= hi || (a.debug & 1)) continue;
+        T* d[1] = {own + lo};
+        const T* sp[1] = {buf[j] + lo};
+        grp_xfer<T, 1, 1, false, false, false, 8>(d, sp, hi - lo, 1.0f, gt, nt);
+      }
+    }
+  }
+  group_publish<W>(a, r, 2, a.seq + 1u, 0, gt, nt, nullptr, 0);
+  group_wait<W>(a, r, 2, a.seq + 1u, 0, gt, nt, nullptr, 0);
+}
+
+template <typename T>
+cudaError_t run_view(const P2PLaunch& a, cudaStream_t st) {
+  P2PLaunch pa = a;
+  void* args[] = {&pa};
+  void* fn = nullptr;
+  switch (a.world) {
+    case 2: fn = reinterpret_cast<void*>(pull_view_twoshot_kernel<T, 2>); break;
+    case 3: fn = reinterpret_cast<void*>(pull_view_twoshot_kernel<T, 3>); break;
+    case 4: fn = reinterpret_cast<void*>(pull_view_twoshot_kernel<T, 4>); break;
+    case 5: fn = reinterpret_cast<void*>(pull_view_twoshot_kernel<T, 5>); break;
+    case 6: fn = reinterpret_cast<void*>(pull_view_twoshot_kernel<T, 6>); break;
+    case 7: fn = reinterpret_cast<void*>(pull_view_twoshot_kernel<T, 7>); break;
+    case 8: fn = reinterpret_cast<void*>(pull_view_twoshot_kernel<T, 8>); break;
+    default: return cudaErrorInvalidValue;
+  }
+  if (a.emulated) return cudaLaunchCooperativeKernel(fn, dim3(a.ctas, a.world), dim3(kThreads), args, 0, st);
+  return cudaLaunchKernel(fn, dim3(a.ctas), dim3(kThreads), args, 0, st);
+}
+
 template <int MAXS>
 SlotArgs<MAXS> make_args(const SlotView& sv) {
   SlotArgs<MAXS> a;
@@ -352,7 +439,20 @@ int occupancy(int algo, int world, int n_slots) {
 }  // namespace
 
 cudaError_t launch_pull(int algo, int dtype, const SlotView& sv, const P2PLaunch& a, cudaStream_t s) {
+  if (a.view) return dtype == 0 ? run_view<float>(a, s) : run_view<__nv_bfloat16>(a, s);
   return dtype == 0 ? dispatch<float>(algo, sv, a, s) : dispatch<__nv_bfloat16>(algo, sv, a, s);
+}
+
+int pull_view_occupancy(int dtype, int world) {
+  int blocks = 0;
+  void* fn = nullptr;
+#define B200DDP_V(WW) \
+  case WW: fn = dtype == 0 ? reinterpret_cast<void*>(pull_view_twoshot_kernel<float, WW>) \
+                           : reinterpret_cast<void*>(pull_view_twoshot_kernel<__nv_bfloat16, WW>); break;
+  switch (world) { B200DDP_V(2) B200DDP_V(3) B200DDP_V(4) B200DDP_V(5) B200DDP_V(6) B200DDP_V(7) B200DDP_V(8) default: return 0; }
+#undef B200DDP_V
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, kThreads, 0) != cudaSuccess) return 0;
+  return blocks;
 }
 
 int pull_occupancy(int algo, int dtype, int world, int n_slots) {

@@ -228,9 +228,10 @@ class DistributedDataParallel(torch.nn.Module):
     storage, so the buckets are averaged in place (``DDP_OPT_GRAD_VIEW``: no
     pack / unpack).  Clear gradients with ``zero_grad(set_to_none=False)`` to
     keep the views; a re-created ``.grad`` is copied into its slot and the view
-    re-attached at the end of the pass.  At world > 2 every bucket then uses the
-    copy-engine two-shot (CE2), the last one included: measured slower than the
-    default policy at W=4 (profiles/r01_grad_view.md), so it trades time for memory.
+    re-attached at the end of the pass.  The buckets synced beside backward then
+    use the copy engines in place (CE at world 2, CE2 wider) under the fp32 overlap
+    policy, the last bucket (and every bucket under the bf16 policy) the fused
+    two-shot in place (include/b200ddp.h, DDP_OPT_GRAD_VIEW).
     The exchange policy for hook-driven passes is ``DDP_OPT_PREFER_OVERLAP``:
     1 (copy engines) for fp32 models, 2 (SM kernels) otherwise, unless
     ``options`` sets it.

@@ -457,19 +457,22 @@ def test_option_and_algo_constants_match_header():
 
 @pytest.mark.parametrize("model,esize", [("resnet50", 4), ("bert_large", 2), ("toy", 4)])
 def test_grad_view_layout(model, esize):
-    """DDP_OPT_GRAD_VIEW (N-3 zero-copy): every bucket is averaged in place (CE
-    at world 2, CE2 wider, NCCL when forced or at world 1); each parameter's slot (ddp_param_storage_offset) sits at its bucket's
+    """DDP_OPT_GRAD_VIEW (N-3 zero-copy): every bucket is averaged in place (the
+    fused two-shot; CE / CE2 when forced or beside a backward under the overlap
+    policy; NCCL when forced or at world 1); each parameter's slot (ddp_param_storage_offset) sits at its bucket's
     base + its element offset (O-1 mapping), inside the storage, slots disjoint
     and in the same order as the oracle's buckets."""
     ns = numels(model)
     cap = 25 * MIB
     ctx = L.ddp_create(ns, L.FP32 if esize == 4 else L.BF16, cap, 4, 1)
     try:
-        L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_TWOSHOT)     # GRAD_VIEW overrides it
+        L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_CE2)
         L.ddp_set_option(ctx, L.OPT_GRAD_VIEW, 1)
         assert L.ddp_get_option(ctx, L.OPT_GRAD_VIEW) == 1
         nb = L.ddp_num_buckets(ctx)
-        assert {L.ddp_bucket_algo(ctx, b) for b in range(nb)} == {L.ALGO_CE2}   # world 4: CE2 in place
+        assert {L.ddp_bucket_algo(ctx, b) for b in range(nb)} == {L.ALGO_CE2}   # forced: CE2 in place
+        L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_AUTO)
+        assert {L.ddp_bucket_algo(ctx, b) for b in range(nb)} == {L.ALGO_TWOSHOT}  # fused two-shot in place
         L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_NCCL)
         assert {L.ddp_bucket_algo(ctx, b) for b in range(nb)} == {L.ALGO_NCCL}
         L.ddp_set_option(ctx, L.OPT_ALGO, L.ALGO_TWOSHOT)
@@ -500,12 +503,21 @@ def test_grad_view_layout(model, esize):
             L.ddp_param_storage_offset(ctx, len(ns))
         L.ddp_set_option(ctx, L.OPT_GRAD_VIEW, 0)
         assert {L.ddp_bucket_algo(ctx, b) for b in range(nb)} == {L.ALGO_TWOSHOT}
-        # world 2: the copy-engine exchange in place, unless NCCL is forced
+        # world 2: the fused two-shot in place (no second buffer, no staging); under the
+        # overlap policy the copy engines beside backward, the fused kernel for the last
+        # bucket; NCCL when forced
         two = L.ddp_create(ns, L.FP32 if esize == 4 else L.BF16, cap, 2, 0)
         try:
             L.ddp_set_option(two, L.OPT_GRAD_VIEW, 1)
-            assert {L.ddp_bucket_algo(two, b) for b in range(nb)} == {L.ALGO_CE}
-            assert L.ddp_storage_bytes(two) >= 3 * sum(ns) * esize   # bucket region + 2 CE slots
+            assert {L.ddp_bucket_algo(two, b) for b in range(nb)} == {L.ALGO_TWOSHOT}
+            in_place = L.ddp_storage_bytes(two)
+            L.ddp_set_option(two, L.OPT_ALGO, L.ALGO_CE)
+            assert L.ddp_storage_bytes(two) >= in_place + 2 * sum(ns) * esize   # CE adds W receive slots
+            L.ddp_set_option(two, L.OPT_ALGO, L.ALGO_AUTO)
+            L.ddp_set_option(two, L.OPT_PREFER_OVERLAP, 1)
+            al = [L.ddp_bucket_algo(two, b) for b in range(nb)]
+            assert al[-1] == L.ALGO_TWOSHOT and set(al[:-1]) <= {L.ALGO_CE}
+            L.ddp_set_option(two, L.OPT_PREFER_OVERLAP, 0)
             L.ddp_set_option(two, L.OPT_ALGO, L.ALGO_NCCL)
             assert {L.ddp_bucket_algo(two, b) for b in range(nb)} == {L.ALGO_NCCL}
         finally:
@@ -530,7 +542,7 @@ def test_grad_view_protocol_unchanged(world):
     L.ddp_set_option(ctx, L.OPT_DRY_RUN, 1)
     rng = random.Random(29 + world)
     try:
-        want = {1: L.ALGO_NCCL, 2: L.ALGO_CE, 4: L.ALGO_CE2}[world]
+        want = {1: L.ALGO_NCCL, 2: L.ALGO_TWOSHOT, 4: L.ALGO_TWOSHOT}[world]
         assert {L.ddp_bucket_algo(ctx, b) for b in range(L.ddp_num_buckets(ctx))} == {want}
         for _ in range(10):
             order = list(range(len(ns)))

@@ -91,7 +91,7 @@ def test_two_ranks_agree_on_launch_order_nccl_id_and_view_layout():
     assert all(lay == layouts[0] for lay in layouts)          # identical slot layout on every rank
     offs, total, algos = layouts[0]
     from paper_2006_15704_b200 import _lib as L
-    assert set(algos) == {L.ALGO_CE}                         # world 2: the copy-engine exchange in place
+    assert set(algos) == {L.ALGO_TWOSHOT}                    # world 2: the fused two-shot in place
     assert len(set(offs)) == len(offs) and max(offs) < total
 
 

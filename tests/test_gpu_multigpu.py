@@ -138,7 +138,7 @@ def test_multigpu_parity(world):
         tol = any(x in ("nccl", "nvls") for x in algos)   # not rank-order sums: tolerance parity
         wire = len(cfg) > 5 and cfg[5].get(L.OPT_WIRE_BF16)
         if len(cfg) > 5 and cfg[5].get(L.OPT_GRAD_VIEW) and algo == L.ALGO_AUTO:
-            assert set(algos) == ({"ce"} if world == 2 else {"ce2"}), algos
+            assert set(algos) == {"twoshot"}, algos             # the fused two-shot in place
         for it in range(iters):
             for p in range(len(ns)):
                 sums = [outs[r][ci][0][it][0][p] for r in range(world)]
