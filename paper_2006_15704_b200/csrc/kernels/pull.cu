@@ -11,9 +11,12 @@
 // exactly oracle O-3b, bit-identical on all ranks.
 //
 // Why pull (vs pushing into peers' staging): a rank signals "my stores are done"
-// only for LOCAL stores (its own buffer), so the system-scope release before
-// each flag drains local HBM writes, not remote NVLink writes; the all-gather
-// reads land straight in .grad (no unpack pass, no closing barrier).  Reuse of a
+// only for LOCAL stores (its own buffer), so a gpu-scope fence before each flag
+// suffices (reading A-1; ~1 us against 5-8 us for the system-scope
+// fence remote stores need); the all-gather reads land straight in .grad (no
+// unpack pass, no closing barrier).  Pulling needs many CTAs to keep enough loads
+// in flight, so by default it runs the last bucket of a pass (every SM); the
+// buckets beside backward keep the push kernels (kernels/p2p.cu).  Reuse of a
 // buffer is ordered by double buffering: pass v uses buffer v % 2 of the bucket,
 // and a rank rewrites buffer v % 2 in pass v + 2 only after its pass-(v+1)
 // kernel saw every peer's pass-(v+1) "packed" flag, which each peer raised
@@ -33,9 +36,10 @@
 //   G  reads chunk c of every other shard j from rank j's buffer (the sums)
 //      straight into .grad.
 // Stages + warp specialization: each CTA chunk is split into `stages` sub-chunks;
-// half of the CTA's warps pack stage after stage (P) and publish each, the other
-// half read and reduce one stage behind (R, G), so local packing overlaps the
-// NVLink reads.
+// a quarter (or half) of the CTA's warps pack stage after stage (P) and publish
+// each, the others read and reduce one stage behind (R, G), so local packing
+// overlaps the NVLink reads.  A third form, pull_view_twoshot_kernel, runs the
+// two-shot in place on gradients that ARE the bucket (DDP_OPT_GRAD_VIEW).
 #include "barrier.cuh"
 
 namespace b200ddp {
