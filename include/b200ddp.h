@@ -10,7 +10,9 @@
  *     pending count per bucket and in-order bucket launch;
  *   - pack + scale by 1/world into the flat bucket;
  *   - bucket allreduce on a communication stream overlapping backward
- *      — NCCL, or a hand-written sm_100a P2P kernel;
+ *      — hand-written sm_100a kernels over NVLink peer
+ *     memory (fused one-shot / two-shot in push or pull form, NVLS), copy-engine
+ *     exchanges ordered by stream memory operations, or NCCL;
  *   - unpack of the averaged values into the gradients;
  *   - no_sync accumulation.
  *
@@ -29,6 +31,10 @@
  *     be reallocated between iterations.  Symmetric storage passed to
  *     ddp_bind_device is caller-allocated and must outlive the context.  The
  *     library owns its NCCL communicator, CUDA events and tables.
+ *   - Ordering: a launched bucket's device work follows everything the
+ *     producer stream(s) of its ready signals had enqueued; the first launch of
+ *     a pass follows the previous pass's end (the event finalize recorded), so
+ *     the library's staging and flags are never reused early.
  *   - State machine: CREATED -> (bind) -> IDLE <-> IN_PASS.  The first
  *     ddp_grad_ready of a pass opens it; ddp_finalize_backward closes it.
  *     A CUDA or NCCL failure, a peer timeout or DDP_ERR_INCOMPLETE poisons
