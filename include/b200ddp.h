@@ -150,8 +150,10 @@ enum {
                                    (%globaltimer); a peer that never arrives makes the waiting CTAs
                                    give up, set the error word and exit -> DDP_ERR_TIMEOUT from
                                    ddp_check_device_errors (poisons).  Default 30000; any time */
-  DDP_OPT_WAIT_TIMEOUT_MS = 21, /* peer emulation (b200ddp_emu.h) only: bound of a host wait for a
-                                   peer's step (default 60000); any time */
+  DDP_OPT_WAIT_TIMEOUT_MS = 21, /* bound of a host wait for a peer's step under peer emulation
+                                   (b200ddp_emu.h), and the host watchdog's bound: a finalized pass not
+                                   complete this long after ddp_finalize_backward is reported by
+                                   ddp_check_device_errors (default 60000); any time */
   DDP_OPT_EMU_DEAD_RANK = 22,   /* test support, cooperative emulation only (ddp_bind_emulated):
                                    this rank's CTAs return at once and never signal, so the others
                                    must time out (DDP_OPT_P2P_TIMEOUT_MS).  -1 (default) = none */
@@ -190,8 +192,10 @@ enum {
  * cuStreamWaitValue32, which has no timeout: a peer that dies mid-pass leaves this
  * rank's library streams (and every stream ordered after them) blocked, exactly
  * as a dead peer leaves an NCCL collective blocked ("the backward pass
- * could hang").  Recovery is process-level: destroy the context (the NCCL
- * communicator is aborted when poisoned) and exit.
+ * could hang").  The host watchdog in ddp_check_device_errors reports such a pass
+ * (DDP_ERR_TIMEOUT, poisoned) once it is DDP_OPT_WAIT_TIMEOUT_MS past its
+ * finalize.  Recovery is process-level: destroy the context (it does not wait for
+ * its streams when poisoned; the NCCL communicator is aborted) and exit.
  *
  *   NCCL:    pack kernel -> ncclAllReduce(sum) -> unpack kernel (DDP_OPT_GRAD_VIEW: in-place
  *            ncclAllReduce(avg) on the slots the gradients live in; no pack / unpack)
@@ -360,7 +364,12 @@ ddp_status_t ddp_ready_order(const ddp_ctx_t* ctx, int32_t* out, int32_t cap, in
  * Errors: DDP_ERR_STATE, DDP_ERR_INVALID_ARG, DDP_ERR_NCCL. */
 ddp_status_t ddp_broadcast(ddp_ctx_t* ctx, void* const* bufs, const int64_t* bytes, int32_t n, int32_t root,
                            void* stream);
-/* Checks the device-side error word (P2P barrier timeout). */
+/* Non-blocking health check; call it from the host between steps.  Reports, in
+ * this order: the device-side error word (a fused kernel's peer wait timed out,
+ * DDP_OPT_P2P_TIMEOUT_MS), an NCCL asynchronous error, and the host watchdog: the
+ * last finalized pass not complete DDP_OPT_WAIT_TIMEOUT_MS after its finalize (a
+ * copy-engine flag wait or a collective stuck on a dead peer).  Each poisons the
+ * context and returns DDP_ERR_TIMEOUT (DDP_ERR_NCCL for the NCCL error). */
 ddp_status_t ddp_check_device_errors(ddp_ctx_t* ctx);
 const char* ddp_last_error(void);
 /* Library version string. */

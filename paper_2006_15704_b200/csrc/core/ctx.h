@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <string>
 #include <utility>
@@ -102,7 +103,8 @@ struct ddp_ctx {
   int64_t prefer_overlap = 0;  // policy for buckets synced under a running backward (see resolve_algo)
   int64_t grad_view = 0;       // N-3 zero-copy: gradients live in their bucket slots (NCCL in place)
   int64_t p2p_timeout_ms = 30000;   // bound of every P2P / NVLS barrier spin (%globaltimer)
-  int64_t wait_timeout_ms = 60000;  // peer emulation: bound of a host wait for a peer's issue
+  int64_t wait_timeout_ms = 60000;  // bound of a host wait for a peer's issue (peer emulation) and
+                                    // of a finalized pass's completion (ddp_check_device_errors)
   int64_t emu_dead_rank = -1;       // test support (cooperative emulation): this rank never signals
   int64_t p2p_pull = 1;             // fused kernels: 0 push everywhere, 1 pull for the last bucket, 2 pull everywhere
   int64_t p2p_signal = 0;           // pull kernels: flag publication mode (DDP_OPT_P2P_SIGNAL)
@@ -150,6 +152,8 @@ struct ddp_ctx {
   bool no_sync = false, pass_no_sync = false;
   bool pass_launched = false;    // a device launch happened in the open pass
   bool comm_done_valid = false;  // comm_done recorded by an earlier finalize
+  bool watch = false;            // comm_done not yet seen complete by ddp_check_device_errors
+  std::chrono::steady_clock::time_point done_since;  // finalize of the oldest pass not seen complete
   std::vector<uint8_t> ready;
   std::vector<int32_t> pending;
   int32_t cursor = 0, n_ready = 0;

@@ -41,6 +41,14 @@ ddp_status_t nccl_fail(ddp_ctx* c, ncclResult_t r, const char* what) {
   return fail(DDP_ERR_NCCL, std::string(what) + ": " + ncclGetErrorString(r));
 }
 
+// The previous pass's end event has completed (or failed: the caller's next
+// check reports that).  cudaErrorNotReady is cleared, not left for the caller.
+static bool pass_complete(ddp_ctx* c) {
+  if (cudaEventQuery(c->comm_done) != cudaErrorNotReady) return true;
+  (void)cudaGetLastError();
+  return false;
+}
+
 }  // namespace b200ddp
 
 namespace {
@@ -836,6 +844,10 @@ ddp_status_t ddp_finalize_backward(ddp_ctx_t* c, void* consumer_stream) {
       // the last bucket ran on its producer stream, after every library stream was
       // joined into it (exchange.cpp): that stream alone marks the end of the pass
       cudaStream_t end = c->last_on ? c->last_on : c->comm;
+      // watchdog (ddp_check_device_errors): time from the finalize of the oldest
+      // pass not yet seen complete; a later pass completes after it (stream order)
+      if (!c->watch || pass_complete(c)) c->done_since = std::chrono::steady_clock::now();
+      c->watch = true;
       CUDA_TRY(c, cudaEventRecord(c->comm_done, end));
       c->comm_done_valid = true;
       c->done_stream = end;
@@ -1117,6 +1129,28 @@ ddp_status_t ddp_check_device_errors(ddp_ctx_t* c) {
     ncclResult_t ar = ncclSuccess;
     if (ncclCommGetAsyncError(c->nccl, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress)
       return nccl_fail(c, ar, "NCCL async error");
+  }
+  // Host watchdog over the waits that have no device-side bound (the copy-engine
+  // exchanges' cuStreamWaitValue32, NCCL): a finalized pass that has not completed
+  // DDP_OPT_WAIT_TIMEOUT_MS later is reported, and the context poisoned, so the
+  // caller can tear down instead of blocking forever ("could hang").
+  if (c->watch) {
+    const cudaError_t q = cudaEventQuery(c->comm_done);
+    if (q == cudaSuccess) {
+      c->watch = false;
+    } else if (q == cudaErrorNotReady) {
+      (void)cudaGetLastError();  // not an error: do not leave it for the caller's next check
+      const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() -
+                                                                            c->done_since).count();
+      if (ms > c->wait_timeout_ms) {
+        c->poisoned = true;
+        return fail(DDP_ERR_TIMEOUT, "a finalized pass has not completed " + std::to_string(ms) +
+                                         " ms after ddp_finalize_backward (a peer never raised a flag this "
+                                         "rank waits on, or a collective is stuck)");
+      }
+    } else {
+      return cuda_fail(c, q, "cudaEventQuery(pass end)");
+    }
   }
   return DDP_OK;
 }

@@ -340,6 +340,42 @@ def test_dead_peer_fused_kernel_rendezvous_times_out():
         pe.close()
 
 
+def test_watchdog_reports_a_pass_that_never_completes():
+    """ddp_check_device_errors' host watchdog over the waits with no device-side
+    bound (copy-engine flags, NCCL): a finalized pass whose end has not completed
+    DDP_OPT_WAIT_TIMEOUT_MS later -> DDP_ERR_TIMEOUT, context poisoned.  Stand-in
+    for a peer that never raises a flag: a ~1.5 s GPU spin ahead of the pass on
+    the producer stream.  A pass that completes in time is never reported."""
+    import time
+    from paper_2006_15704_b200.ddp import GradReducer
+    ns = numels("toy")
+    red = GradReducer(ns, "fp32", 4096, options={L.OPT_WAIT_TIMEOUT_MS: 200})
+    try:
+        grads = [torch.ones(n, device="cuda") for n in ns]
+        for p in range(len(ns) - 1, -1, -1):   # a pass that completes: no report
+            red.grad_ready(p, grads[p])
+        red.finalize()
+        red.check_errors()
+        torch.cuda.synchronize()
+        time.sleep(0.3)
+        red.check_errors()
+        torch.cuda._sleep(3_000_000_000)        # holds the producer stream ~1.5 s
+        for p in range(len(ns) - 1, -1, -1):
+            red.grad_ready(p, grads[p])
+        red.finalize()
+        red.check_errors()                      # within the bound
+        time.sleep(0.5)
+        with pytest.raises(L.DDPError) as e:
+            red.check_errors()
+        assert e.value.status == L.ERR_TIMEOUT and "has not completed" in str(e.value)
+        torch.cuda.synchronize()
+        with pytest.raises(L.DDPError) as e:
+            red.grad_ready(0, grads[0])
+        assert e.value.status == L.ERR_POISONED
+    finally:
+        red.close()
+
+
 @pytest.mark.parametrize("algo", [L.ALGO_ONESHOT, L.ALGO_TWOSHOT])
 def test_dead_peer_in_kernel_barrier_times_out(algo):
     """Cooperative emulation with rank 1's CTAs absent (DDP_OPT_EMU_DEAD_RANK):
