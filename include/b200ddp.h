@@ -74,10 +74,11 @@ enum {
   DDP_OPT_OVERLAP = 1,          /* 1 (default): launch buckets from the hooks; 0: launch all at
                                    finalize — the non-overlapped baseline of P:L164-L175 / L399 */
   DDP_OPT_P2P_ONESHOT_MAX = 2,  /* buckets <= this many bytes use the one-shot P2P kernel (default
-                                   1 MiB); larger ones the world-dependent default (world 2: one-shot
-                                   with the pull kernels (CE with the push kernels), world > 2:
-                                   two-shot) */
-  DDP_OPT_P2P_TWOSHOT_MAX = 3,  /* buckets larger than this many bytes use NCCL (default: none) */
+                                   -1 = automatic: 1 MiB; settable >= 0); larger ones the
+                                   world-dependent default (world 2: one-shot with the pull kernels
+                                   (CE with the push kernels), world > 2: two-shot) */
+  DDP_OPT_P2P_TWOSHOT_MAX = 3,  /* buckets larger than this many bytes use NCCL (default INT64_MAX:
+                                   none) */
   DDP_OPT_COMM_CTAS = 4,        /* max CTAs of a P2P kernel when world > 1 (1..148, default 32);
                                    the last bucket of a pass always runs on 148 */
   DDP_OPT_DRY_RUN = 5,          /* 1: protocol only, no device work (host tests; CREATED only) */

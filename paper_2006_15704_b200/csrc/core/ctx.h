@@ -82,7 +82,7 @@ struct ddp_ctx {
   std::vector<int32_t> p_bucket, p_slot;
   std::vector<int64_t> p_off;
   // options
-  // oneshot_max < 0: automatic (world 2: <= 1 MiB; world > 2: <= 512 KiB)
+  // oneshot_max < 0: automatic (<= 1 MiB at every world size)
   int64_t overlap = 1, oneshot_max = -1, twoshot_max = INT64_MAX,
           comm_ctas = 32,  // x 4 lanes: measured best exposed time at W=4 (profiles/r01_n4.md)
           dry_run = 0, profile = 0, algo = DDP_ALGO_AUTO,

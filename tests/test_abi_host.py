@@ -550,3 +550,54 @@ def test_grad_view_protocol_unchanged(world):
             assert _run_pass(ctx, order) == replay(a, order)
     finally:
         L.ddp_destroy(ctx)
+
+
+# Defaults as include/b200ddp.h documents them, and the accepted range of every
+# bounded option (one below / the bounds / one above).
+_DEFAULTS = {
+    "OVERLAP": 1, "P2P_ONESHOT_MAX": -1, "P2P_TWOSHOT_MAX": 2**63 - 1, "COMM_CTAS": 32, "DRY_RUN": 0,
+    "PROFILE": 0, "ALGO": 0, "PACK_CTAS": 4736, "P2P_STAGE_BYTES": 0, "FIND_UNUSED": 0, "MULTICAST": 0,
+    "CE_STREAMS": 1, "NCCL_COMMS": 1, "CE_DIRECT_BYTES": 16 * MIB, "WIRE_BF16": 0, "LANES": 4,
+    "LOW_PRIORITY": 1, "PREFER_OVERLAP": 0, "GRAD_VIEW": 0, "P2P_TIMEOUT_MS": 30000, "WAIT_TIMEOUT_MS": 60000,
+    "EMU_DEAD_RANK": -1, "P2P_PULL": 1, "P2P_SIGNAL": 0, "P2P_DEBUG": 0, "LAST_ON_PRODUCER": 1,
+}
+_RANGES = {  # name: (lowest legal, highest legal or None = unbounded)
+    "ALGO": (0, 7), "PREFER_OVERLAP": (0, 2), "LANES": (1, 4), "CE_STREAMS": (1, 16), "NCCL_COMMS": (1, 8),
+    "COMM_CTAS": (1, 148), "PACK_CTAS": (1, 148 * 64), "P2P_PULL": (0, 2), "P2P_SIGNAL": (0, 3),
+    "P2P_DEBUG": (0, 7), "EMU_DEAD_RANK": (-1, 1), "P2P_ONESHOT_MAX": (0, None), "P2P_TWOSHOT_MAX": (0, None),
+    "CE_DIRECT_BYTES": (0, None), "P2P_STAGE_BYTES": (0, None), "P2P_TIMEOUT_MS": (1, None),
+    "WAIT_TIMEOUT_MS": (1, None),
+}
+_BOOLEANS = ("OVERLAP", "PROFILE", "DRY_RUN", "FIND_UNUSED", "MULTICAST", "WIRE_BF16", "LOW_PRIORITY",
+             "GRAD_VIEW", "LAST_ON_PRODUCER")
+
+
+def test_option_defaults_ranges_and_booleans():
+    keys = {n[4:]: getattr(L, n) for n in dir(L) if n.startswith("OPT_")}
+    assert set(keys) == set(_DEFAULTS)
+    ctx = L.ddp_create([3, 4], L.FP32, 10, 2, 0)
+    try:
+        for name, want in _DEFAULTS.items():
+            assert L.ddp_get_option(ctx, keys[name]) == want, name
+    finally:
+        L.ddp_destroy(ctx)
+
+    def accepted(name, v):
+        c = L.ddp_create([3, 4], L.FP32, 10, 2, 0)
+        try:
+            L.ddp_set_option(c, keys[name], v)
+            return L.ddp_get_option(c, keys[name])
+        except L.DDPError as e:
+            assert e.status == L.ERR_INVALID_ARG, (name, v)
+            return None
+        finally:
+            L.ddp_destroy(c)
+
+    for name, (lo, hi) in _RANGES.items():
+        assert accepted(name, lo - 1) is None, name
+        assert accepted(name, lo) == lo, name
+        if hi is not None:
+            assert accepted(name, hi) == hi, name
+            assert accepted(name, hi + 1) is None, name
+    for name in _BOOLEANS:                       # any non-zero value reads back as 1
+        assert accepted(name, 2) == 1 and accepted(name, 0) == 0, name
