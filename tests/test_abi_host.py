@@ -601,3 +601,19 @@ def test_option_defaults_ranges_and_booleans():
             assert accepted(name, hi + 1) is None, name
     for name in _BOOLEANS:                       # any non-zero value reads back as 1
         assert accepted(name, 2) == 1 and accepted(name, 0) == 0, name
+
+
+def test_product_path_has_no_fallback(monkeypatch):
+    """The product path fails loudly without its native library (no CPU or
+    oracle fallback), and nothing in the package or the C/CUDA sources refers to
+    oracle/ (the oracle is test infrastructure only)."""
+    monkeypatch.setattr(L, "_lib", None)
+    monkeypatch.setattr(L, "LIB_PATH", os.path.join(ROOT, "no-such-dir", "libb200ddp.so"))
+    with pytest.raises(ImportError, match="no fallback"):
+        L.ddp_version()
+    pkg = os.path.join(ROOT, "paper_2006_15704_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
+                txt = open(os.path.join(dirpath, f), errors="replace").read()
+                assert not re.search(r"^\s*(from|import)\s+oracle\b|#include\s*[<\"][^>\"]*oracle", txt, re.M), f
